@@ -1,0 +1,303 @@
+"""MicroMix (arXiv 2508.02343) hot path on B200 -- thin Python binding.
+
+Argument marshalling only: every step of the path runs in the sm_100a kernels of
+libmicromix_b200.so behind the C ABI in include/mm.h.  PyTorch provides device
+memory and the current CUDA stream; there is no CPU fallback -- if the library
+is missing or the device is not sm_100, calls raise.
+
+Functions carry the C names:
+    mm_plan_init, mm_calibrate_thresholds, mm_quantize_weight_offline,
+    mm_reorder_quantize_act, mm_mixed_gemm_bf16, mm_reorder_act_bf16,
+    mm_comm_init, mm_mixed_gemm_bf16_nshard_allgather.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmicromix_b200.so")
+
+MM_E2M1, MM_E3M2, MM_E2M3, MM_E4M3, MM_E5M2 = range(5)
+MM_SCALE_OCP, MM_SCALE_PAPER_EQ1 = 0, 1
+STATUS = {0: "MM_OK", 1: "MM_ERR_INVALID_ARGUMENT", 2: "MM_ERR_SHAPE", 3: "MM_ERR_ALIGNMENT",
+          4: "MM_ERR_PLAN_MISMATCH", 5: "MM_ERR_DEGENERATE", 6: "MM_ERR_UNSUPPORTED_DEVICE",
+          7: "MM_ERR_CUDA", 8: "MM_ERR_NCCL", 9: "MM_ERR_WORKSPACE"}
+SEG_BITS = (4, 6, 8)
+
+# Every symbol include/mm.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "mm_padded_cols", "mm_code_pitch_bytes", "mm_codes_bytes", "mm_sf_bytes",
+    "mm_calib_workspace_bytes", "mm_plan_init", "mm_calibrate_thresholds",
+    "mm_quantize_weight_offline", "mm_reorder_quantize_act", "mm_mixed_gemm_bf16",
+    "mm_reorder_act_bf16", "mm_set_gemm_config", "mm_launch_count", "mm_reset_launch_count",
+    "mm_last_error", "mm_abi_version", "mm_nccl_unique_id_bytes", "mm_nccl_get_unique_id",
+    "mm_comm_init", "mm_comm_destroy", "mm_mixed_gemm_bf16_nshard_allgather",
+]
+
+
+class MMError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class CPlan(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int32), ("n", ctypes.c_int32 * 3), ("fmt6", ctypes.c_int32),
+                ("fmt8", ctypes.c_int32), ("rule", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("d_perm", ctypes.c_void_p), ("fingerprint", ctypes.c_uint64),
+                ("tensor_max", ctypes.c_double), ("t4", ctypes.c_double), ("t6", ctypes.c_double),
+                ("c", ctypes.c_int32 * 3), ("reserved2", ctypes.c_int32)]
+
+
+class CMx(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("codes", ctypes.c_void_p * 3), ("sf", ctypes.c_void_p * 3),
+                ("fingerprint", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def lib(build_if_missing: bool = False):
+    """The loaded CUDA library; raises if it is not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            if build_if_missing:
+                from .build import build
+                build()
+            else:
+                raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                                   "(python -m paper_2508_02343_b200.build)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+        P, X = ctypes.POINTER(CPlan), ctypes.POINTER(CMx)
+        sig = {
+            "mm_padded_cols": (i64, [P, ctypes.c_int]),
+            "mm_code_pitch_bytes": (i64, [P, ctypes.c_int]),
+            "mm_codes_bytes": (i64, [P, i64, ctypes.c_int]),
+            "mm_sf_bytes": (i64, [P, i64, ctypes.c_int]),
+            "mm_calib_workspace_bytes": (i64, [i64, i32]),
+            "mm_plan_init": (ctypes.c_int, [P, i32, ctypes.POINTER(i32), i32, i32, i32, vp, vp, vp]),
+            "mm_calibrate_thresholds": (ctypes.c_int, [vp, i64, i32, i64, i32, i32, i32, vp, P, vp,
+                                                       ctypes.c_size_t, vp, vp, vp]),
+            "mm_quantize_weight_offline": (ctypes.c_int, [vp, i64, i64, P, X, vp]),
+            "mm_reorder_quantize_act": (ctypes.c_int, [vp, i64, i64, P, X, vp]),
+            "mm_mixed_gemm_bf16": (ctypes.c_int, [X, X, P, vp, i64, vp]),
+            "mm_reorder_act_bf16": (ctypes.c_int, [vp, i64, i64, P, vp, i64, vp]),
+            "mm_set_gemm_config": (ctypes.c_int, [i32, i32, i32]),
+            "mm_launch_count": (i64, []),
+            "mm_reset_launch_count": (None, []),
+            "mm_last_error": (ctypes.c_char_p, []),
+            "mm_abi_version": (i32, []),
+            "mm_nccl_unique_id_bytes": (i32, []),
+            "mm_nccl_get_unique_id": (ctypes.c_int, [vp]),
+            "mm_comm_init": (ctypes.c_int, [i32, i32, vp, ctypes.POINTER(vp)]),
+            "mm_comm_destroy": (ctypes.c_int, [vp]),
+            "mm_mixed_gemm_bf16_nshard_allgather": (ctypes.c_int, [X, X, P, i64, vp, i64, vp, vp, vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise MMError(st, lib().mm_last_error().decode())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else ctypes.c_void_p(0)
+
+
+class Plan:
+    """A channel plan (include/mm.h mm_plan) plus the device permutation it borrows."""
+
+    def __init__(self, c: CPlan, d_perm: torch.Tensor):
+        self.c = c
+        self.d_perm = d_perm
+
+    @property
+    def K(self):
+        return self.c.K
+
+    @property
+    def n(self):
+        return tuple(self.c.n)
+
+    @property
+    def fmt6(self):
+        return self.c.fmt6
+
+    @property
+    def fmt8(self):
+        return self.c.fmt8
+
+    @property
+    def rule(self):
+        return self.c.rule
+
+    def padded_cols(self, g):
+        return lib().mm_padded_cols(ctypes.byref(self.c), g)
+
+    def pitch(self, g):
+        return lib().mm_code_pitch_bytes(ctypes.byref(self.c), g)
+
+    def codes_bytes(self, rows, g):
+        return lib().mm_codes_bytes(ctypes.byref(self.c), rows, g)
+
+    def sf_bytes(self, rows, g):
+        return lib().mm_sf_bytes(ctypes.byref(self.c), rows, g)
+
+    def perm_host(self):
+        return self.d_perm.cpu()
+
+
+class MXTensor:
+    """A quantized operand: per-segment packed codes and E8M0 scale atoms (uint8 buffers)."""
+
+    def __init__(self, plan: Plan, rows: int, device=None):
+        device = device or plan.d_perm.device
+        self.plan = plan
+        self.rows = rows
+        self.codes, self.sf = [], []
+        c = CMx()
+        c.rows = rows
+        for g in range(3):
+            if plan.n[g] == 0:
+                self.codes.append(None)
+                self.sf.append(None)
+                continue
+            cb = torch.empty(max(plan.codes_bytes(rows, g), 1), dtype=torch.uint8, device=device)
+            sb = torch.empty(max(plan.sf_bytes(rows, g), 1), dtype=torch.uint8, device=device)
+            self.codes.append(cb)
+            self.sf.append(sb)
+            c.codes[g] = cb.data_ptr()
+            c.sf[g] = sb.data_ptr()
+        self.c = c
+
+    def codes2d(self, g):
+        return self.codes[g][: self.plan.codes_bytes(self.rows, g)].view(self.rows, self.plan.pitch(g))
+
+
+def mm_plan_init(K, n, perm, fmt6=MM_E3M2, fmt8=MM_E4M3, rule=MM_SCALE_OCP, device="cuda") -> Plan:
+    perm = torch.as_tensor(perm, dtype=torch.int32).contiguous().cpu()
+    d_perm = torch.empty(K, dtype=torch.int32, device=device)
+    c = CPlan()
+    nn = (ctypes.c_int32 * 3)(*[int(v) for v in n])
+    _check(lib().mm_plan_init(ctypes.byref(c), K, nn, fmt6, fmt8, rule, ctypes.c_void_p(perm.data_ptr()),
+                              _ptr(d_perm), _stream()))
+    return Plan(c, d_perm)
+
+
+def mm_calibrate_thresholds(x: torch.Tensor, fmt6=MM_E3M2, fmt8=MM_E4M3, rule=MM_SCALE_OCP,
+                            return_stats=False):
+    assert x.dtype == torch.bfloat16 and x.dim() == 2 and x.stride(1) == 1
+    L, K = x.shape
+    d_perm = torch.empty(K, dtype=torch.int32, device=x.device)
+    ws = torch.empty(max(lib().mm_calib_workspace_bytes(L, K), 1), dtype=torch.uint8, device=x.device)
+    chmax = torch.empty(K, dtype=torch.float64)
+    chmean = torch.empty(K, dtype=torch.float64)
+    c = CPlan()
+    _check(lib().mm_calibrate_thresholds(_ptr(x), L, K, x.stride(0), fmt6, fmt8, rule, _ptr(d_perm),
+                                         ctypes.byref(c), _ptr(ws), ws.numel(),
+                                         ctypes.c_void_p(chmax.data_ptr()), ctypes.c_void_p(chmean.data_ptr()),
+                                         _stream()))
+    plan = Plan(c, d_perm)
+    return (plan, chmax, chmean) if return_stats else plan
+
+
+def _rq(fn, x: torch.Tensor, plan: Plan, out: MXTensor | None, stream=None) -> MXTensor:
+    assert x.dtype == torch.bfloat16 and x.dim() == 2 and x.stride(1) == 1
+    rows = x.shape[0]
+    if out is None:
+        out = MXTensor(plan, rows, x.device)
+    _check(fn(_ptr(x), rows, x.stride(0), ctypes.byref(plan.c), ctypes.byref(out.c), _stream(stream)))
+    return out
+
+
+def mm_quantize_weight_offline(w: torch.Tensor, plan: Plan, out: MXTensor | None = None, stream=None):
+    return _rq(lib().mm_quantize_weight_offline, w, plan, out, stream)
+
+
+def mm_reorder_quantize_act(x: torch.Tensor, plan: Plan, out: MXTensor | None = None, stream=None):
+    return _rq(lib().mm_reorder_quantize_act, x, plan, out, stream)
+
+
+def mm_mixed_gemm_bf16(a: MXTensor, w: MXTensor, plan: Plan, out: torch.Tensor | None = None,
+                       stream=None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(a.rows, w.rows, dtype=torch.bfloat16, device=plan.d_perm.device)
+    assert out.dtype == torch.bfloat16 and out.stride(1) == 1
+    _check(lib().mm_mixed_gemm_bf16(ctypes.byref(a.c), ctypes.byref(w.c), ctypes.byref(plan.c), _ptr(out),
+                                    out.stride(0), _stream(stream)))
+    return out
+
+
+def mm_reorder_act_bf16(x: torch.Tensor, plan: Plan) -> torch.Tensor:
+    out = torch.empty_like(x)
+    _check(lib().mm_reorder_act_bf16(_ptr(x), x.shape[0], x.stride(0), ctypes.byref(plan.c), _ptr(out),
+                                     out.stride(0), _stream()))
+    return out
+
+
+def mm_set_gemm_config(block_n=0, num_stages=0, max_ctas=0):
+    _check(lib().mm_set_gemm_config(block_n, num_stages, max_ctas))
+
+
+def launch_count() -> int:
+    return lib().mm_launch_count()
+
+
+def reset_launch_count():
+    lib().mm_reset_launch_count()
+
+
+# ---- multi-GPU -------------------------------------------------------------------
+def nccl_unique_id() -> bytes:
+    n = lib().mm_nccl_unique_id_bytes()
+    buf = ctypes.create_string_buffer(n)
+    _check(lib().mm_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+def mm_comm_init(rank: int, world: int, unique_id: bytes):
+    buf = ctypes.create_string_buffer(unique_id, len(unique_id))
+    comm = ctypes.c_void_p()
+    _check(lib().mm_comm_init(rank, world, buf, ctypes.byref(comm)))
+    return comm
+
+
+def mm_comm_destroy(comm):
+    _check(lib().mm_comm_destroy(comm))
+
+
+def mm_mixed_gemm_bf16_nshard_allgather(a: MXTensor, w_shard: MXTensor, plan: Plan, n_total: int, comm,
+                                        out: torch.Tensor | None = None, stage: torch.Tensor | None = None):
+    dev = plan.d_perm.device
+    if out is None:
+        out = torch.empty(a.rows, n_total, dtype=torch.bfloat16, device=dev)
+    if stage is None:
+        stage = torch.empty(a.rows * n_total, dtype=torch.bfloat16, device=dev)
+    _check(lib().mm_mixed_gemm_bf16_nshard_allgather(ctypes.byref(a.c), ctypes.byref(w_shard.c),
+                                                     ctypes.byref(plan.c), n_total, _ptr(out), out.stride(0),
+                                                     _ptr(stage), comm, _stream()))
+    return out
+
+
+def shard_rows(N: int, world: int, rank: int):
+    """Rows of W owned by `rank` under N-sharding (host logic, CPU-testable)."""
+    if N % world:
+        raise ValueError("N must divide evenly across ranks")
+    ns = N // world
+    return rank * ns, (rank + 1) * ns

@@ -1,0 +1,62 @@
+// comm.cu -- N-sharding support: layout of the all-gathered BF16 shards and the
+// NCCL binding (loaded at run time; the torch-bundled libnccl.so.2 is reused
+// when torch already loaded it).  DESIGN.md "Multi-GPU".
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <mutex>
+
+#include "internal.h"
+
+namespace mmx {
+namespace {
+
+// stage [G][M][Ns] (BF16) -> y [M][ldy], 16-byte vectors (Ns % 8 == 0).
+__global__ void gather_layout_kernel(const uint4* __restrict__ stage, int G, int64_t M, int64_t Ns8,
+                                     uint16_t* __restrict__ y, int64_t ldy) {
+  const int64_t total = (int64_t)G * M * Ns8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c8 = i % Ns8;
+    const int64_t m = (i / Ns8) % M;
+    const int64_t g = i / (Ns8 * M);
+    *reinterpret_cast<uint4*>(y + m * ldy + (g * Ns8 + c8) * 8) = __ldcs(stage + i);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_gather_layout(const uint16_t* stage, int G, int64_t M, int64_t Ns, uint16_t* y,
+                                 int64_t ldy, cudaStream_t s, int64_t* launches) {
+  const int64_t total = (int64_t)G * M * (Ns / 8);
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 8 * sm_count()) blocks = 8 * sm_count();
+  gather_layout_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(stage), G, M, Ns / 8, y,
+                                                        ldy);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+// ---- NCCL, resolved with dlopen ------------------------------------------------
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.getUniqueId = reinterpret_cast<decltype(&ncclGetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(&ncclCommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.commDestroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.allGather = reinterpret_cast<decltype(&ncclAllGather)>(dlsym(h, "ncclAllGather"));
+    api.errStr = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allGather && api.errStr;
+  });
+  return api;
+}
+
+}  // namespace mmx

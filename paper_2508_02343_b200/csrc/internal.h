@@ -1,0 +1,84 @@
+// internal.h -- launch interfaces between the C-ABI layer (mm_api.cpp) and the
+// sm_100a kernels.  Not part of the public ABI (that is include/mm.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <cstdint>
+
+namespace mmx {
+
+enum : int { F_E2M1 = 0, F_E3M2 = 1, F_E2M3 = 2, F_E4M3 = 3, F_E5M2 = 4 };
+
+// Geometry of one quantized operand derived from a plan (see include/mm.h).
+struct SegGeom {
+  int n[3];        // channels per segment
+  int kp[3];       // stored (padded) columns per segment = roundup(n, 128)
+  int off[3];      // start of the segment in the reordered channel order
+  int fmt[3];      // element format per segment
+  int sc_off[3];   // Eq. 1 exponent offset per segment (emax or bias)
+  int64_t pitch[3];  // code bytes per row
+};
+
+struct RqArgs {
+  const uint16_t* x;   // BF16 bits [rows, ldx]
+  int64_t rows;
+  int64_t ldx;
+  int K;
+  const int32_t* perm; // device int32[K]
+  SegGeom geom;
+  uint8_t* codes[3];
+  uint8_t* sf[3];
+};
+
+// Fused reorder-and-quantize (rq.cu).
+cudaError_t launch_reorder_quantize(const RqArgs& a, cudaStream_t s, int64_t* launches);
+// Test entry: gathered BF16 x_r (rq.cu).
+cudaError_t launch_reorder_bf16(const uint16_t* x, int64_t rows, int64_t ldx, int K,
+                                const int32_t* perm, uint16_t* xr, int64_t ldxr,
+                                cudaStream_t s, int64_t* launches);
+
+// Calibration statistics (calib.cu): chmax (double), chmean (double) on device.
+size_t calib_workspace_bytes(int64_t L, int K);
+cudaError_t launch_calib_stats(const uint16_t* x, int64_t L, int64_t ldx, int K,
+                               void* ws, double* d_chmax, double* d_chmean,
+                               cudaStream_t s, int64_t* launches);
+
+struct GemmArgs {
+  int64_t M, N;
+  SegGeom geom;
+  const uint8_t* a_codes[3];
+  const uint8_t* a_sf[3];
+  const uint8_t* w_codes[3];
+  const uint8_t* w_sf[3];
+  uint16_t* y;   // BF16 [M, ldy]
+  int64_t ldy;
+};
+
+struct GemmConfig {
+  int block_n = 0;      // 0 = auto
+  int num_stages = 0;   // 0 = auto
+  int max_ctas = 0;     // 0 = #SMs
+};
+
+// Mixed block-scaled GEMM (gemm.cu).
+cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s,
+                              int64_t* launches, const char** err);
+
+// [G][M][Ns] -> [M][G*Ns] layout fix after the all-gather (comm.cu).
+cudaError_t launch_gather_layout(const uint16_t* stage, int G, int64_t M, int64_t Ns,
+                                 uint16_t* y, int64_t ldy, cudaStream_t s, int64_t* launches);
+
+int sm_count();
+
+// NCCL entry points resolved with dlopen (comm.cu).
+struct NcclApi {
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllGather) allGather = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+  bool ok = false;
+};
+const NcclApi& nccl();
+
+}  // namespace mmx

@@ -1,0 +1,474 @@
+// mm_api.cpp -- the C ABI of include/mm.h: argument validation, plan geometry,
+// fingerprints, the host half of calibration (thresholds, counts, argsort), and
+// dispatch to the sm_100a kernels.  Citations: include/mm.h and DESIGN.md.
+#include "../../include/mm.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace mmx {
+
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+GemmConfig g_gemm_cfg;
+std::mutex g_cfg_mu;
+
+mm_status fail(mm_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+mm_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(MM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+mm_status check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(MM_ERR_UNSUPPORTED_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a (B200)", dev,
+                major, minor);
+  return MM_OK;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int64_t roundup(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+int bits_of(int g) { return g == 0 ? 4 : (g == 1 ? 6 : 8); }
+
+int emax_of(int fmt) {
+  switch (fmt) {
+    case F_E2M1: return 2;
+    case F_E3M2: return 4;
+    case F_E2M3: return 2;
+    case F_E4M3: return 8;
+    default: return 15;  // E5M2
+  }
+}
+int bias_of(int fmt) {
+  switch (fmt) {
+    case F_E2M1: return 1;
+    case F_E3M2: return 3;
+    case F_E2M3: return 1;
+    case F_E4M3: return 7;
+    default: return 15;
+  }
+}
+double qmax_of(int fmt) {
+  switch (fmt) {
+    case F_E2M1: return 6.0;
+    case F_E3M2: return 28.0;
+    case F_E2M3: return 7.5;
+    case F_E4M3: return 448.0;
+    default: return 57344.0;
+  }
+}
+
+mm_status validate_plan_fields(int32_t K, const int32_t n[3], int32_t fmt6, int32_t fmt8, int32_t rule) {
+  if (K < 32 || K % 32 != 0 || K > 65536) return fail(MM_ERR_SHAPE, "K=%d must be a multiple of 32 in [32, 65536]", K);
+  int64_t s = 0;
+  for (int g = 0; g < 3; ++g) {
+    if (n[g] < 0 || n[g] % 32 != 0) return fail(MM_ERR_SHAPE, "n[%d]=%d must be a non-negative multiple of 32", g, n[g]);
+    s += n[g];
+  }
+  if (s != K) return fail(MM_ERR_SHAPE, "n4+n6+n8=%lld != K=%d", (long long)s, K);
+  if (fmt6 != MM_E3M2 && fmt6 != MM_E2M3) return fail(MM_ERR_INVALID_ARGUMENT, "fmt6 must be E3M2 or E2M3");
+  if (fmt8 != MM_E4M3 && fmt8 != MM_E5M2) return fail(MM_ERR_INVALID_ARGUMENT, "fmt8 must be E4M3 or E5M2");
+  if (rule != MM_SCALE_OCP && rule != MM_SCALE_PAPER_EQ1) return fail(MM_ERR_INVALID_ARGUMENT, "bad scale rule");
+  return MM_OK;
+}
+
+mm_status validate_plan(const mm_plan* p) {
+  if (!p) return fail(MM_ERR_INVALID_ARGUMENT, "plan is NULL");
+  mm_status st = validate_plan_fields(p->K, p->n, p->fmt6, p->fmt8, p->rule);
+  if (st != MM_OK) return st;
+  if (!p->d_perm) return fail(MM_ERR_INVALID_ARGUMENT, "plan.d_perm is NULL");
+  return MM_OK;
+}
+
+SegGeom geom_of(const mm_plan* p) {
+  SegGeom G{};
+  const int fmts[3] = {F_E2M1, p->fmt6, p->fmt8};
+  int off = 0;
+  for (int g = 0; g < 3; ++g) {
+    G.n[g] = p->n[g];
+    G.kp[g] = (int)roundup(p->n[g], 128);
+    G.off[g] = off;
+    off += p->n[g];
+    G.fmt[g] = fmts[g];
+    G.sc_off[g] = p->rule == MM_SCALE_OCP ? emax_of(fmts[g]) : bias_of(fmts[g]);
+    G.pitch[g] = (int64_t)G.kp[g] * bits_of(g) / 8;
+  }
+  return G;
+}
+
+uint64_t fingerprint(int32_t K, const int32_t n[3], int32_t fmt6, int32_t fmt8, int32_t rule, const int32_t* perm) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint32_t v) {
+    for (int i = 0; i < 4; ++i) {
+      h ^= (v >> (8 * i)) & 0xFF;
+      h *= 1099511628211ull;
+    }
+  };
+  mix((uint32_t)K);
+  for (int g = 0; g < 3; ++g) mix((uint32_t)n[g]);
+  mix((uint32_t)fmt6);
+  mix((uint32_t)fmt8);
+  mix((uint32_t)rule);
+  for (int32_t k = 0; k < K; ++k) mix((uint32_t)perm[k]);
+  return h | 1ull;  // never 0 (0 = "no plan")
+}
+
+// Shared memory the reorder-quantize kernel needs for this K (R = 1 layout).
+bool rq_fits(int32_t K) { return (size_t)K * 2 * 3 + 256 <= 220 * 1024; }
+
+mm_status check_mx_out(const mm_plan* p, const mm_mx_tensor* t, int64_t rows, const char* what) {
+  if (!t) return fail(MM_ERR_INVALID_ARGUMENT, "%s is NULL", what);
+  for (int g = 0; g < 3; ++g) {
+    if (p->n[g] == 0) continue;
+    if (!t->codes[g] || !t->sf[g]) return fail(MM_ERR_INVALID_ARGUMENT, "%s segment %d buffers are NULL", what, g);
+    if (!aligned(t->codes[g], 256) || !aligned(t->sf[g], 256))
+      return fail(MM_ERR_ALIGNMENT, "%s segment %d buffers must be 256-byte aligned", what, g);
+  }
+  (void)rows;
+  return MM_OK;
+}
+
+mm_status run_rq(const void* d_x, int64_t rows, int64_t ldx, const mm_plan* plan, mm_mx_tensor* out,
+                 mm_stream_t stream, const char* what) {
+  mm_status st = check_device();
+  if (st != MM_OK) return st;
+  if ((st = validate_plan(plan)) != MM_OK) return st;
+  if (rows < 0) return fail(MM_ERR_SHAPE, "rows < 0");
+  if (!d_x && rows > 0) return fail(MM_ERR_INVALID_ARGUMENT, "input is NULL");
+  if (ldx < plan->K) return fail(MM_ERR_SHAPE, "ld=%lld < K=%d", (long long)ldx, plan->K);
+  if (ldx % 8 != 0 || !aligned(d_x, 16)) return fail(MM_ERR_ALIGNMENT, "input rows must be 16-byte aligned");
+  if (!rq_fits(plan->K)) return fail(MM_ERR_SHAPE, "K=%d exceeds the shared-memory capacity of the RQ kernel", plan->K);
+  if ((st = check_mx_out(plan, out, rows, what)) != MM_OK) return st;
+  out->rows = rows;
+  out->fingerprint = plan->fingerprint;
+  if (rows == 0) return MM_OK;
+  RqArgs a{};
+  a.x = static_cast<const uint16_t*>(d_x);
+  a.rows = rows;
+  a.ldx = ldx;
+  a.K = plan->K;
+  a.perm = plan->d_perm;
+  a.geom = geom_of(plan);
+  for (int g = 0; g < 3; ++g) {
+    a.codes[g] = static_cast<uint8_t*>(out->codes[g]);
+    a.sf[g] = static_cast<uint8_t*>(out->sf[g]);
+  }
+  cudaError_t e = launch_reorder_quantize(a, reinterpret_cast<cudaStream_t>(stream), &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "reorder-quantize launch");
+  return MM_OK;
+}
+
+}  // namespace
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 1;
+  }
+  return cached[dev];
+}
+
+}  // namespace mmx
+
+using namespace mmx;
+
+extern "C" {
+
+int32_t mm_abi_version(void) { return 1; }
+const char* mm_last_error(void) { return g_err.c_str(); }
+int64_t mm_launch_count(void) { return g_launches; }
+void mm_reset_launch_count(void) { g_launches = 0; }
+
+int64_t mm_padded_cols(const mm_plan* p, int seg) {
+  if (!p || seg < 0 || seg > 2 || p->n[seg] < 0) return -1;
+  return roundup(p->n[seg], 128);
+}
+int64_t mm_code_pitch_bytes(const mm_plan* p, int seg) {
+  int64_t kp = mm_padded_cols(p, seg);
+  return kp < 0 ? -1 : kp * bits_of(seg) / 8;
+}
+int64_t mm_codes_bytes(const mm_plan* p, int64_t rows, int seg) {
+  int64_t pitch = mm_code_pitch_bytes(p, seg);
+  return (pitch < 0 || rows < 0) ? -1 : rows * pitch;
+}
+int64_t mm_sf_bytes(const mm_plan* p, int64_t rows, int seg) {
+  int64_t kp = mm_padded_cols(p, seg);
+  return (kp < 0 || rows < 0) ? -1 : roundup(rows, 128) * kp / 32;
+}
+int64_t mm_calib_workspace_bytes(int64_t L, int32_t K) {
+  if (L < 0 || K <= 0) return -1;
+  return (int64_t)roundup((int64_t)calib_workspace_bytes(L, K), 256) + 2 * (int64_t)roundup((int64_t)K * 8, 256);
+}
+
+mm_status mm_set_gemm_config(int32_t block_n, int32_t num_stages, int32_t max_ctas) {
+  if (block_n != 0 && block_n != 128 && block_n != 256) return fail(MM_ERR_INVALID_ARGUMENT, "block_n must be 0/128/256");
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  g_gemm_cfg.block_n = block_n;
+  g_gemm_cfg.num_stages = num_stages;
+  g_gemm_cfg.max_ctas = max_ctas;
+  return MM_OK;
+}
+
+mm_status mm_plan_init(mm_plan* out, int32_t K, const int32_t n[3], int32_t fmt6, int32_t fmt8, int32_t rule,
+                       const int32_t* h_perm, int32_t* d_perm_storage, mm_stream_t stream) {
+  if (!out || !n || !h_perm || !d_perm_storage) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  mm_status st = validate_plan_fields(K, n, fmt6, fmt8, rule);
+  if (st != MM_OK) return st;
+  std::vector<char> seen(K, 0);
+  for (int32_t j = 0; j < K; ++j) {
+    if (h_perm[j] < 0 || h_perm[j] >= K || seen[h_perm[j]])
+      return fail(MM_ERR_INVALID_ARGUMENT, "permutation is not a bijection on [0, K) (position %d)", j);
+    seen[h_perm[j]] = 1;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(d_perm_storage, h_perm, (size_t)K * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "copy permutation");
+  std::memset(out, 0, sizeof(*out));
+  out->K = K;
+  for (int g = 0; g < 3; ++g) out->n[g] = n[g];
+  out->fmt6 = fmt6;
+  out->fmt8 = fmt8;
+  out->rule = rule;
+  out->d_perm = d_perm_storage;
+  out->fingerprint = fingerprint(K, n, fmt6, fmt8, rule, h_perm);
+  return MM_OK;
+}
+
+mm_status mm_calibrate_thresholds(const void* d_x, int64_t L, int32_t K, int64_t ldx, int32_t fmt6, int32_t fmt8,
+                                  int32_t rule, int32_t* d_perm_out, mm_plan* plan_out, void* d_ws, size_t ws_bytes,
+                                  double* h_chmax, double* h_chmean, mm_stream_t stream) {
+  mm_status st = check_device();
+  if (st != MM_OK) return st;
+  const int32_t nz[3] = {K, 0, 0};
+  if ((st = validate_plan_fields(K, nz, fmt6, fmt8, rule)) != MM_OK) return st;
+  if (!d_x || !d_perm_out || !plan_out || !d_ws) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (L <= 0) return fail(MM_ERR_SHAPE, "L must be positive");
+  if (ldx < K) return fail(MM_ERR_SHAPE, "ldx < K");
+  if (ldx % 8 != 0 || !aligned(d_x, 16)) return fail(MM_ERR_ALIGNMENT, "input rows must be 16-byte aligned");
+  if ((int64_t)ws_bytes < mm_calib_workspace_bytes(L, K) || !aligned(d_ws, 256))
+    return fail(MM_ERR_WORKSPACE, "workspace too small or unaligned (need %lld bytes)",
+                (long long)mm_calib_workspace_bytes(L, K));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(d_ws);
+  const int64_t part_bytes = roundup((int64_t)calib_workspace_bytes(L, K), 256);
+  double* d_chmax = reinterpret_cast<double*>(ws + part_bytes);
+  double* d_chmean = reinterpret_cast<double*>(ws + part_bytes + roundup((int64_t)K * 8, 256));
+  cudaError_t e = launch_calib_stats(static_cast<const uint16_t*>(d_x), L, ldx, K, ws, d_chmax, d_chmean, s,
+                                     &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "calibration launch");
+  std::vector<double> chmax(K), chmean(K);
+  e = cudaMemcpyAsync(chmax.data(), d_chmax, (size_t)K * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(chmean.data(), d_chmean, (size_t)K * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "calibration statistics");
+  // Eq. 5: T(n) = 2^(b+n-1) max|X| / (254 q_max), one correctly rounded division.
+  double tmax = 0.0;
+  for (double v : chmax) tmax = std::max(tmax, v);
+  if (!(tmax > 0.0)) return fail(MM_ERR_DEGENERATE, "calibration data has max|X| == 0");
+  const double t4 = (std::ldexp(1.0, bias_of(F_E2M1) + 4 - 1) * tmax) / (254.0 * qmax_of(F_E2M1));
+  const double t6 = (std::ldexp(1.0, bias_of(fmt6) + 6 - 1) * tmax) / (254.0 * qmax_of(fmt6));
+  // Eq. 6 / Eq. 17: channel counts by channel max.
+  int32_t c4 = 0, c6 = 0;
+  for (double v : chmax) {
+    if (v <= t4) ++c4;
+    else if (v <= t6) ++c6;
+  }
+  const int32_t c8 = K - c4 - c6;
+  // Rounding to whole 32-blocks: n8 up, then n6 up (capped), n4 the remainder.
+  int32_t n[3];
+  n[2] = (int32_t)roundup(c8, 32);
+  n[1] = std::min((int32_t)roundup(c6, 32), K - n[2]);
+  n[0] = K - n[2] - n[1];
+  // Eq. 7 + Q3: stable ascending argsort of the channel means.
+  std::vector<int32_t> perm(K);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return chmean[a] < chmean[b]; });
+  if ((st = mm_plan_init(plan_out, K, n, fmt6, fmt8, rule, perm.data(), d_perm_out, stream)) != MM_OK) return st;
+  plan_out->tensor_max = tmax;
+  plan_out->t4 = t4;
+  plan_out->t6 = t6;
+  plan_out->c[0] = c4;
+  plan_out->c[1] = c6;
+  plan_out->c[2] = c8;
+  if (h_chmax) std::memcpy(h_chmax, chmax.data(), (size_t)K * 8);
+  if (h_chmean) std::memcpy(h_chmean, chmean.data(), (size_t)K * 8);
+  return MM_OK;
+}
+
+mm_status mm_quantize_weight_offline(const void* d_w, int64_t N, int64_t ldw, const mm_plan* plan,
+                                     mm_mx_tensor* w_out, mm_stream_t stream) {
+  return run_rq(d_w, N, ldw, plan, w_out, stream, "w_out");
+}
+
+mm_status mm_reorder_quantize_act(const void* d_x, int64_t M, int64_t ldx, const mm_plan* plan, mm_mx_tensor* a_out,
+                                  mm_stream_t stream) {
+  return run_rq(d_x, M, ldx, plan, a_out, stream, "a_out");
+}
+
+mm_status mm_reorder_act_bf16(const void* d_x, int64_t M, int64_t ldx, const mm_plan* plan, void* d_xr,
+                              int64_t ldxr, mm_stream_t stream) {
+  mm_status st = check_device();
+  if (st != MM_OK) return st;
+  if ((st = validate_plan(plan)) != MM_OK) return st;
+  if (M < 0 || ldx < plan->K || ldxr < plan->K) return fail(MM_ERR_SHAPE, "bad shape");
+  if (M > 0 && (!d_x || !d_xr)) return fail(MM_ERR_INVALID_ARGUMENT, "NULL buffer");
+  cudaError_t e = launch_reorder_bf16(static_cast<const uint16_t*>(d_x), M, ldx, plan->K, plan->d_perm,
+                                      static_cast<uint16_t*>(d_xr), ldxr, reinterpret_cast<cudaStream_t>(stream),
+                                      &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "reorder launch");
+  return MM_OK;
+}
+
+static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const mm_plan* plan, void* d_y,
+                             int64_t ldy, int64_t n_cols, mm_stream_t stream) {
+  mm_status st = check_device();
+  if (st != MM_OK) return st;
+  if ((st = validate_plan(plan)) != MM_OK) return st;
+  if (!a || !w) return fail(MM_ERR_INVALID_ARGUMENT, "operand is NULL");
+  if (a->fingerprint != plan->fingerprint || w->fingerprint != plan->fingerprint)
+    return fail(MM_ERR_PLAN_MISMATCH, "operands were not produced with this plan");
+  if ((st = check_mx_out(plan, a, a->rows, "a")) != MM_OK) return st;
+  if ((st = check_mx_out(plan, w, w->rows, "w")) != MM_OK) return st;
+  const int64_t M = a->rows, N = w->rows;
+  if (M < 0 || N < 0) return fail(MM_ERR_SHAPE, "negative rows");
+  if (N % 16 != 0) return fail(MM_ERR_SHAPE, "N=%lld must be a multiple of 16", (long long)N);
+  if (ldy < n_cols || ldy % 8 != 0) return fail(MM_ERR_SHAPE, "ldy=%lld must be >= N and a multiple of 8", (long long)ldy);
+  if (M > 0 && N > 0 && (!d_y || !aligned(d_y, 16))) return fail(MM_ERR_ALIGNMENT, "Y must be 16-byte aligned");
+  if (M == 0 || N == 0) return MM_OK;
+  GemmArgs ga{};
+  ga.M = M;
+  ga.N = N;
+  ga.geom = geom_of(plan);
+  for (int g = 0; g < 3; ++g) {
+    ga.a_codes[g] = static_cast<const uint8_t*>(a->codes[g]);
+    ga.a_sf[g] = static_cast<const uint8_t*>(a->sf[g]);
+    ga.w_codes[g] = static_cast<const uint8_t*>(w->codes[g]);
+    ga.w_sf[g] = static_cast<const uint8_t*>(w->sf[g]);
+  }
+  ga.y = static_cast<uint16_t*>(d_y);
+  ga.ldy = ldy;
+  GemmConfig cfg;
+  {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    cfg = g_gemm_cfg;
+  }
+  const char* err = "";
+  cudaError_t e = launch_mixed_gemm(ga, cfg, reinterpret_cast<cudaStream_t>(stream), &g_launches, &err);
+  if (e != cudaSuccess) return fail(MM_ERR_CUDA, "mixed GEMM launch: %s (%s)", cudaGetErrorString(e), err);
+  return MM_OK;
+}
+
+mm_status mm_mixed_gemm_bf16(const mm_mx_tensor* a, const mm_mx_tensor* w, const mm_plan* plan, void* d_y,
+                             int64_t ldy, mm_stream_t stream) {
+  return gemm_common(a, w, plan, d_y, ldy, w ? w->rows : 0, stream);
+}
+
+// ---------------------------------------------------------------- multi-GPU
+struct MmComm {
+  ncclComm_t comm;
+  int rank, world;
+};
+
+int32_t mm_nccl_unique_id_bytes(void) { return (int32_t)sizeof(ncclUniqueId); }
+
+mm_status mm_nccl_get_unique_id(void* h_id_out) {
+  if (!h_id_out) return fail(MM_ERR_INVALID_ARGUMENT, "NULL id buffer");
+  const NcclApi& api = nccl();
+  if (!api.ok) return fail(MM_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  ncclResult_t r = api.getUniqueId(&id);
+  if (r != ncclSuccess) return fail(MM_ERR_NCCL, "ncclGetUniqueId: %s", api.errStr(r));
+  std::memcpy(h_id_out, &id, sizeof(id));
+  return MM_OK;
+}
+
+mm_status mm_comm_init(int32_t rank, int32_t world, const void* h_unique_id, void** comm_out) {
+  if (!h_unique_id || !comm_out) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(MM_ERR_INVALID_ARGUMENT, "bad rank/world");
+  const NcclApi& api = nccl();
+  if (!api.ok) return fail(MM_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  std::memcpy(&id, h_unique_id, sizeof(id));
+  MmComm* c = new MmComm{nullptr, rank, world};
+  ncclResult_t r = api.commInitRank(&c->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(MM_ERR_NCCL, "ncclCommInitRank: %s", api.errStr(r));
+  }
+  *comm_out = c;
+  return MM_OK;
+}
+
+mm_status mm_comm_destroy(void* comm) {
+  if (!comm) return MM_OK;
+  MmComm* c = static_cast<MmComm*>(comm);
+  const NcclApi& api = nccl();
+  if (api.ok && c->comm) api.commDestroy(c->comm);
+  delete c;
+  return MM_OK;
+}
+
+mm_status mm_mixed_gemm_bf16_nshard_allgather(const mm_mx_tensor* a, const mm_mx_tensor* w_shard,
+                                              const mm_plan* plan, int64_t n_total, void* d_y_full, int64_t ldy,
+                                              void* d_stage, void* comm, mm_stream_t stream) {
+  if (!comm || !d_stage || !a || !w_shard) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  MmComm* c = static_cast<MmComm*>(comm);
+  const int64_t Ns = w_shard->rows;
+  if (Ns * c->world != n_total) return fail(MM_ERR_SHAPE, "shard rows * world != n_total");
+  if (Ns % 16 != 0) return fail(MM_ERR_SHAPE, "shard rows must be a multiple of 16");
+  if (ldy < n_total || ldy % 8 != 0) return fail(MM_ERR_SHAPE, "bad ldy");
+  if (!aligned(d_stage, 16)) return fail(MM_ERR_ALIGNMENT, "stage must be 16-byte aligned");
+  const int64_t M = a->rows;
+  uint16_t* stage = static_cast<uint16_t*>(d_stage);
+  uint16_t* mine = stage + (int64_t)c->rank * M * Ns;
+  mm_status st = gemm_common(a, w_shard, plan, mine, Ns, Ns, stream);
+  if (st != MM_OK) return st;
+  if (M == 0 || Ns == 0) return MM_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const NcclApi& api = nccl();
+  if (!api.ok) return fail(MM_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclResult_t r = api.allGather(mine, stage, (size_t)(M * Ns), ncclBfloat16, c->comm, s);
+  if (r != ncclSuccess) return fail(MM_ERR_NCCL, "ncclAllGather: %s", api.errStr(r));
+  cudaError_t e = launch_gather_layout(stage, c->world, M, Ns, static_cast<uint16_t*>(d_y_full), ldy, s, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "layout launch");
+  return MM_OK;
+}
+
+}  // extern "C"

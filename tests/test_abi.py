@@ -1,0 +1,85 @@
+"""CPU checks of the C ABI: the library builds/loads and exports every symbol
+include/mm.h declares; size queries and host-side validation (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+import paper_2508_02343_b200 as mm
+
+
+def _header_symbols():
+    txt = open(os.path.join(ROOT, "include", "mm.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    names = set(re.findall(r"\b(mm_[a-z0-9_]+)\s*\(", txt))
+    return sorted(names)
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2508_02343_b200.build import build
+    build()
+    return mm.lib()
+
+
+def test_header_matches_binding_list():
+    assert sorted(mm.EXPORTS) == _header_symbols()
+
+
+def test_library_exports_every_symbol(L):
+    for name in _header_symbols():
+        assert hasattr(L, name), name
+    assert L.mm_abi_version() == 1
+
+
+def _plan(K, n, fmt6=mm.MM_E3M2, fmt8=mm.MM_E4M3):
+    c = mm.CPlan()
+    c.K = K
+    for i in range(3):
+        c.n[i] = n[i]
+    c.fmt6, c.fmt8 = fmt6, fmt8
+    return c
+
+
+def test_size_queries(L):
+    c = _plan(4096, (2240, 1184, 672))
+    p = ctypes.byref(c)
+    assert [L.mm_padded_cols(p, g) for g in range(3)] == [2304, 1280, 768]
+    assert [L.mm_code_pitch_bytes(p, g) for g in range(3)] == [1152, 960, 768]
+    assert L.mm_codes_bytes(p, 2048, 1) == 2048 * 960
+    assert L.mm_sf_bytes(p, 2000, 0) == 2048 * 2304 // 32
+    assert L.mm_sf_bytes(p, 16, 2) == 128 * 768 // 32
+    assert L.mm_padded_cols(p, 3) == -1
+    assert L.mm_calib_workspace_bytes(16384, 4096) > 0
+
+
+def test_plan_init_validation_on_host(L):
+    c = mm.CPlan()
+    n = (ctypes.c_int32 * 3)(64, 32, 32)
+    perm = (ctypes.c_int32 * 128)(*([0] * 128))     # not a bijection
+    st = L.mm_plan_init(ctypes.byref(c), 128, n, mm.MM_E3M2, mm.MM_E4M3, 0, perm, ctypes.c_void_p(16), None)
+    assert st == 1 and b"bijection" in L.mm_last_error()
+    bad_n = (ctypes.c_int32 * 3)(64, 30, 34)
+    st = L.mm_plan_init(ctypes.byref(c), 128, bad_n, mm.MM_E3M2, mm.MM_E4M3, 0, perm, ctypes.c_void_p(16), None)
+    assert st == 2
+    st = L.mm_plan_init(ctypes.byref(c), 128, n, mm.MM_E4M3, mm.MM_E4M3, 0, perm, ctypes.c_void_p(16), None)
+    assert st == 1
+
+
+def test_calls_fail_loudly_without_gpu(L):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    c = _plan(128, (64, 32, 32))
+    x = mm.CMx()
+    st = L.mm_reorder_quantize_act(ctypes.c_void_p(0), 4, 128, ctypes.byref(c), ctypes.byref(x), None)
+    assert st != 0
+
+
+def test_shard_rows_host_logic():
+    assert mm.shard_rows(8192, 8, 3) == (3072, 4096)
+    with pytest.raises(ValueError):
+        mm.shard_rows(100, 8, 0)

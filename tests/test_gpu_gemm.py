@@ -1,0 +1,178 @@
+"""GPU parity: the mixed block-scaled GEMM (mm_mixed_gemm_bf16) vs the fp64 oracle.
+
+Bar (BASELINE.json north_star): relative Frobenius error <= 2e-3 against the
+oracle's fp64 GEMM of the dequantized operands; bit-exact on the exact-integer
+special case (P-I(i)); one-hot probes pin the packed layouts (P-L)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import gemm as ogemm
+from oracle import mx as omx
+from oracle.formats import E2M3, E3M2, E4M3, E5M2
+import paper_2508_02343_b200 as mm
+from synth import bf16_bits, bits_to_bf16, gen_act, gen_perm, gen_weight
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3
+FMT_O = {mm.MM_E3M2: E3M2, mm.MM_E2M3: E2M3, mm.MM_E4M3: E4M3, mm.MM_E5M2: E5M2}
+
+
+def _run(x, w, plan):
+    a = mm.mm_reorder_quantize_act(x.cuda(), plan)
+    wq = mm.mm_quantize_weight_offline(w.cuda(), plan)
+    y = mm.mm_mixed_gemm_bf16(a, wq, plan)
+    torch.cuda.synchronize()
+    return y
+
+
+def _ref(x, w, plan, rows=None, cols=None):
+    return ogemm.mixed_linear_ref(bf16_bits(x), bf16_bits(w), plan.perm_host().numpy(), plan.n,
+                                  FMT_O[plan.fmt6], FMT_O[plan.fmt8], plan.rule, rows=rows, cols=cols)
+
+
+def _check(y, yref, ybf):
+    yg = y.double().cpu().numpy()
+    err = ogemm.rel_fro(yg, yref)
+    assert err <= TOL, err
+    return err
+
+
+def test_cfg1():
+    x = gen_act(16, 256, 1000, 2001)
+    w = gen_weight(256, 256, 3000)
+    plan = mm.mm_plan_init(256, (128, 64, 64), gen_perm(256, 11))
+    y = _run(x, w, plan)
+    yref, ybf = _ref(x, w, plan)
+    _check(y, yref, ybf)
+
+
+def _int_operand(rows, n, rng, kind):
+    """Integer values exactly representable in each segment format, with the
+    block max fixed so that e = 0 under the OCP rule."""
+    n4, n6, n8 = n
+    parts = []
+    if n4:
+        v = rng.choice([-6, -4, -3, -2, -1, 0, 1, 2, 3, 4, 6], size=(rows, n4))
+        v[:, ::32] = 6
+        parts.append(v)
+    if n6:
+        v = rng.choice([-28, -12, -7, -5, -3, -1, 0, 1, 2, 5, 8, 10, 14, 20, 24], size=(rows, n6))
+        v[:, ::32] = 28
+        parts.append(v)
+    if n8:
+        v = rng.integers(-15, 16, size=(rows, n8))
+        v[:, ::32] = 256
+        parts.append(v)
+    return np.concatenate(parts, axis=1).astype(np.float64)
+
+
+@pytest.mark.parametrize("M,N,n", [(128, 256, (256, 128, 128)), (200, 272, (96, 160, 224)),
+                                   (64, 512, (1024, 512, 256))])
+def test_exact_integer_case_bit_exact(M, N, n):
+    """P-I(i): all products and partial sums are integers < 2^24, so FP32
+    accumulation is exact in any order and Y must equal bf16(Y_exact) bit for bit."""
+    rng = np.random.default_rng(M + N)
+    K = sum(n)
+    perm = rng.permutation(K)
+    xa_r = _int_operand(M, n, rng, "a")
+    wa_r = _int_operand(N, n, rng, "w")
+    xa = np.empty_like(xa_r); xa[:, perm] = xa_r      # un-reorder: X[:, perm[j]] = xr[:, j]
+    wa = np.empty_like(wa_r); wa[:, perm] = wa_r
+    x = bits_to_bf16(omx.bf16_rne_bits(xa))
+    w = bits_to_bf16(omx.bf16_rne_bits(wa))
+    plan = mm.mm_plan_init(K, n, perm)
+    y = _run(x, w, plan)
+    exact = xa_r @ wa_r.T
+    assert np.max(np.abs(exact)) < 2 ** 24
+    yref, ybf = _ref(x, w, plan)
+    assert np.array_equal(yref, exact)
+    got = bf16_bits(y.cpu())
+    want = omx.bf16_rne_bits(exact)
+    bad = np.argwhere(got != want)
+    assert len(bad) == 0, (len(bad), bad[:5], y.cpu().double().numpy()[tuple(bad[0])], exact[tuple(bad[0])])
+
+
+@pytest.mark.parametrize("seg", [0, 1, 2])
+def test_one_hot_layout_probe(seg):
+    """P-L: row m of A is one-hot at reordered column j(m) (value 1.0, exact in
+    every format); W has distinct small integers per column, so Y[m, :] reveals
+    which column the tensor core decoded -- pins FP4 nibble order, FP6 bit order
+    and the scale-atom addressing."""
+    n = [0, 0, 0]
+    n[seg] = 256
+    K = 256
+    M, N = 128, 256
+    perm = np.arange(K)
+    rng = np.random.default_rng(seg)
+    jsel = rng.permutation(K)[:M]
+    xa = np.zeros((M, K))
+    xa[np.arange(M), jsel] = 1.0
+    # W[n, j]: integers in [1, 6] with block max 6 (FP4), 28 (FP6), 256 (FP8)
+    wa = rng.choice([1.0, 2.0, 3.0, 4.0], size=(N, K))
+    top = (6.0, 28.0, 256.0)[seg]
+    wa[:, ::32] = top
+    plan = mm.mm_plan_init(K, tuple(n), perm)
+    y = _run(bits_to_bf16(omx.bf16_rne_bits(xa)), bits_to_bf16(omx.bf16_rne_bits(wa)), plan)
+    yc = y.double().cpu().numpy()
+    decoded = [int(np.argmin(np.abs(wa.T - yc[m][None, :]).sum(axis=1))) for m in range(M)]
+    mism = [(m, jsel[m], decoded[m]) for m in range(M) if decoded[m] != jsel[m]]
+    assert not mism, f"segment {seg}: (row, expected col, decoded col) {mism[:8]}"
+
+
+@pytest.mark.parametrize("M,N,n", [(200, 272, (96, 160, 224)), (257, 384, (2240, 1184, 672)),
+                                   (1000, 1024, (0, 0, 512)), (333, 160, (512, 0, 0)),
+                                   (130, 256, (0, 512, 0))])
+def test_random_ragged(M, N, n):
+    K = sum(n)
+    x = gen_act(M, K, 1001, 2000 + M)
+    w = gen_weight(N, K, 3001 + N)
+    plan = mm.mm_plan_init(K, n, gen_perm(K, 12))
+    y = _run(x, w, plan)
+    yref, ybf = _ref(x, w, plan)
+    _check(y, yref, ybf)
+
+
+@pytest.mark.parametrize("fmt6,fmt8,rule", [(mm.MM_E2M3, mm.MM_E5M2, 0), (mm.MM_E3M2, mm.MM_E4M3, 1)])
+def test_variants(fmt6, fmt8, rule):
+    K, n = 1024, (512, 256, 256)
+    x = gen_act(256, K, 1002, 2010)
+    w = gen_weight(512, K, 3010)
+    plan = mm.mm_plan_init(K, n, gen_perm(K, 13), fmt6=fmt6, fmt8=fmt8, rule=rule)
+    y = _run(x, w, plan)
+    yref, ybf = _ref(x, w, plan)
+    _check(y, yref, ybf)
+
+
+@pytest.mark.parametrize("bn,stages", [(128, 6), (256, 4)])
+def test_qproj_full_size(bn, stages):
+    """Config 2, Llama-3.1-8B q_proj, calibrated plan, full fp64 oracle."""
+    mm.mm_set_gemm_config(bn, stages, 0)
+    try:
+        plan = mm.mm_calibrate_thresholds(gen_act(4096, 4096, 1000, 2000).cuda())
+        x = gen_act(2048, 4096, 1000, 2001)
+        w = gen_weight(4096, 4096, 3000)
+        y = _run(x, w, plan)
+        yref, ybf = _ref(x, w, plan)
+        _check(y, yref, ybf)
+    finally:
+        mm.mm_set_gemm_config(0, 0, 0)
+
+
+def test_llama70b_down_sampled():
+    """Config 4 shape (M=8192, K=28672, N=8192) on 1 GPU, 48 sampled rows x 192
+    sampled columns against the oracle."""
+    dev = "cuda"
+    plan = mm.mm_calibrate_thresholds(gen_act(2048, 28672, 1000, 2000, device=dev))
+    x = gen_act(8192, 28672, 1000, 2001, device=dev)
+    w = gen_weight(8192, 28672, 3000, device=dev)
+    y = _run(x, w, plan)
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(8192, 48, replace=False))
+    cols = np.sort(rng.choice(8192, 192, replace=False))
+    xs = x[torch.from_numpy(rows).cuda()].cpu()
+    ws = w[torch.from_numpy(cols).cuda()].cpu()
+    yref, ybf = _ref(xs, ws, plan)
+    ys = y[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()]
+    _check(ys, yref, ybf)

@@ -1,0 +1,150 @@
+"""GPU parity: fused reorder-and-quantize (mm_reorder_quantize_act /
+mm_quantize_weight_offline) vs the oracle, bit-exact on codes, scales,
+padding and the reorder output (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+import torch
+
+from layout import decode_operand
+from oracle import calib as ocal
+from oracle import mx as omx
+from oracle.formats import E2M3, E3M2, E4M3, E5M2
+import paper_2508_02343_b200 as mm
+from synth import bf16_bits, gen_act, gen_perm, gen_uniform_bf16, gen_weight
+
+pytestmark = pytest.mark.gpu
+
+FMT_O = {mm.MM_E3M2: E3M2, mm.MM_E2M3: E2M3, mm.MM_E4M3: E4M3, mm.MM_E5M2: E5M2}
+
+
+def _parity(x: torch.Tensor, plan: mm.Plan, weight=False, rows_sample=None):
+    xg = x.cuda()
+    q = (mm.mm_quantize_weight_offline if weight else mm.mm_reorder_quantize_act)(xg, plan)
+    torch.cuda.synchronize()
+    codes, scales, pads = decode_operand(q, plan.n)
+    bits = bf16_bits(x)
+    perm = plan.perm_host().numpy()
+    if rows_sample is not None:
+        bits = bits[rows_sample]
+        codes = [c[rows_sample] for c in codes]
+        scales = [s[rows_sample] for s in scales]
+    oc, osf, _ = omx.reorder_quantize(bits, perm, plan.n, FMT_O[plan.fmt6], FMT_O[plan.fmt8], plan.rule)
+    for g in range(3):
+        assert np.array_equal(codes[g], oc[g]), f"codes seg {g}: {np.argwhere(codes[g] != oc[g])[:5]}"
+        assert np.array_equal(scales[g], osf[g]), f"scales seg {g}"
+        cpad, spad_c, spad_r = pads[g]
+        assert not np.any(cpad) and not np.any(spad_c) and not np.any(spad_r), f"padding seg {g}"
+
+
+def _fixed_plan(K, n, seed=1, **kw):
+    return mm.mm_plan_init(K, n, gen_perm(K, seed), **kw)
+
+
+def test_cfg1_fixed_split():
+    """BASELINE config 1: M=16, K=256, 128/64/64, 4 outlier channels; perm from
+    the oracle's calibration of a 2048-row draw (ascending channel means)."""
+    cal = ocal.calibrate(bf16_bits(gen_act(2048, 256, 1000, 2000)))
+    assert cal["n"] == (128, 64, 64)
+    plan = mm.mm_plan_init(256, (128, 64, 64), cal["perm"])
+    _parity(gen_act(16, 256, 1000, 2001), plan)
+    plan_p = mm.mm_plan_init(256, (128, 64, 64), cal["perm"], rule=mm.MM_SCALE_PAPER_EQ1)
+    _parity(gen_act(16, 256, 1000, 2001), plan_p)
+
+
+@pytest.mark.parametrize("M", [1, 3, 5, 127, 129, 300])
+def test_ragged_rows(M):
+    plan = _fixed_plan(512, (224, 96, 192), seed=2)
+    _parity(gen_act(M, 512, 1001, 2002 + M), plan)
+
+
+@pytest.mark.parametrize("n", [(256, 0, 0), (0, 256, 0), (0, 0, 256), (32, 32, 192), (160, 0, 96)])
+def test_segment_shapes(n):
+    plan = _fixed_plan(256, n, seed=3)
+    _parity(gen_act(70, 256, 1002, 2100), plan)
+
+
+@pytest.mark.parametrize("fmt6,fmt8,rule", [(mm.MM_E2M3, mm.MM_E5M2, 0), (mm.MM_E2M3, mm.MM_E4M3, 1),
+                                            (mm.MM_E3M2, mm.MM_E5M2, 1)])
+def test_format_variants_and_rules(fmt6, fmt8, rule):
+    plan = _fixed_plan(1024, (512, 288, 224), seed=4, fmt6=fmt6, fmt8=fmt8, rule=rule)
+    _parity(gen_act(130, 1024, 1003, 2200), plan)
+
+
+@pytest.mark.parametrize("K", [4096, 14336, 28672])
+def test_llama_widths_calibrated(K):
+    """The three tile widths (R = 4 / 2 / 1 rows per tile) on calibrated plans."""
+    cal_x = gen_act(1024, K, 1000, 2000)
+    plan = mm.mm_calibrate_thresholds(cal_x.cuda())
+    rows = 2048 if K == 4096 else 256
+    x = gen_act(rows, K, 1000, 2001)
+    _parity(x, plan)
+
+
+def test_qproj_full_size_activation_and_weight():
+    """Config 2 (Llama-3.1-8B q_proj): X[2048, 4096] and W[4096, 4096], full parity."""
+    plan = mm.mm_calibrate_thresholds(gen_act(4096, 4096, 1000, 2000).cuda())
+    _parity(gen_act(2048, 4096, 1000, 2001), plan)
+    _parity(gen_weight(4096, 4096, 3000), plan, weight=True)
+
+
+def test_exhaustive_bf16_times_scales():
+    """Every finite BF16 magnitude (both signs) as an element of blocks whose
+    amax sets e in {-127 (subnormal amax), -60, 0, +60, +120}: 5 x 65280
+    values per format, one plan per segment format."""
+    vals = np.arange(0, 0x7F80, dtype=np.uint16)
+    for amax_bits in (0x0001, 0x2180, 0x3F80, 0x5D80, 0x7B00):
+        amax = omx.bf16_to_f64(np.array([amax_bits], np.uint16))[0]
+        v = vals[omx.bf16_to_f64(vals) <= amax]
+        per = 31
+        nblk = (len(v) + per - 1) // per
+        blocks = np.zeros((nblk, 32), np.uint16)
+        blocks[:, 0] = amax_bits
+        flat = np.zeros(nblk * per, np.uint16)
+        flat[: len(v)] = v
+        flat[1::2] |= 0x8000                     # negative half
+        blocks[:, 1:] = flat.reshape(nblk, per)
+        K = 256
+        rows = (nblk * 32 + K - 1) // K
+        buf = np.zeros(rows * K, np.uint16)
+        buf[: nblk * 32] = blocks.ravel()
+        x = torch.from_numpy(buf.view(np.int16).reshape(rows, K)).view(torch.bfloat16)
+        for n, fmt6, fmt8 in (((256, 0, 0), mm.MM_E3M2, mm.MM_E4M3), ((0, 256, 0), mm.MM_E3M2, mm.MM_E4M3),
+                              ((0, 256, 0), mm.MM_E2M3, mm.MM_E4M3), ((0, 0, 256), mm.MM_E3M2, mm.MM_E4M3),
+                              ((0, 0, 256), mm.MM_E3M2, mm.MM_E5M2)):
+            plan = mm.mm_plan_init(K, n, np.arange(K), fmt6=fmt6, fmt8=fmt8)
+            _parity(x, plan)
+
+
+def test_reorder_output_bit_exact():
+    plan = _fixed_plan(4096, (2048, 1024, 1024), seed=5)
+    x = gen_act(257, 4096, 1004, 2300)
+    xr = mm.mm_reorder_act_bf16(x.cuda(), plan)
+    ref = omx.reorder(bf16_bits(x), plan.perm_host().numpy())
+    assert np.array_equal(bf16_bits(xr), ref)
+
+
+def test_strided_input_and_zero_rows():
+    plan = _fixed_plan(256, (128, 64, 64), seed=6)
+    big = gen_act(40, 512, 1005, 2400)
+    xs = big.cuda()[:, 128:384]                    # ld = 512, offset 256 bytes
+    q = mm.mm_reorder_quantize_act(xs, plan)
+    torch.cuda.synchronize()
+    codes, scales, _ = decode_operand(q, plan.n)
+    oc, osf, _ = omx.reorder_quantize(bf16_bits(big[:, 128:384]), plan.perm_host().numpy(), plan.n)
+    for g in range(3):
+        assert np.array_equal(codes[g], oc[g]) and np.array_equal(scales[g], osf[g])
+    q0 = mm.mm_reorder_quantize_act(torch.empty(0, 256, dtype=torch.bfloat16, device="cuda"), plan)
+    assert q0.rows == 0
+
+
+def test_errors_are_loud():
+    plan = _fixed_plan(256, (128, 64, 64), seed=7)
+    x = gen_act(8, 256, 1006, 2500).cuda()
+    with pytest.raises(mm.MMError):
+        mm.mm_reorder_quantize_act(x[:, 1:], plan)       # misaligned rows
+    other = _fixed_plan(256, (128, 64, 64), seed=8)
+    a = mm.mm_reorder_quantize_act(x, plan)
+    w = mm.mm_quantize_weight_offline(gen_weight(32, 256).cuda(), other)
+    with pytest.raises(mm.MMError) as e:
+        mm.mm_mixed_gemm_bf16(a, w, plan)
+    assert e.value.status == 4
