@@ -1,0 +1,433 @@
+"""bench.py -- one step of the MicroMix hot path on B200, timed.
+
+A STEP is one pass of the whole hot path over one batch of synthetic input:
+    mm_reorder_quantize_act(X)  (fused gather + MX block quantization, rows R1-R5)
+    mm_mixed_gemm_bf16(A, W)    (3-segment block-scaled tcgen05 GEMM, rows R7-R8)
+against offline-calibrated, offline-quantized weights (rows R0, R6; untimed).
+
+Default workload (BASELINE.json configs[1]): Llama-3.1-8B q_proj, M=2048 K=4096
+N=4096, calibrated plan, 1 GPU.  At N>1 GPUs every rank runs its own batch through
+the same layer (data-parallel replicas, weak scaling, no collective);
+`--config llama70b_down` instead N-shards the 70B down_proj over the ranks with
+the library's NCCL all-gather of the BF16 outputs (strong scaling).
+
+L2 policy: every step reads a different one of `nsets` rotating input sets
+(activations, quantized weights, outputs) whose total exceeds 2x the 126 MB L2,
+so no step finds its operands L2-resident from the previous one.
+
+`--impl reference` times the CPU oracle (oracle/, the deliberately slow
+reference of this tier) on a bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "mixed MX GEMM TFLOPS (% mix-weighted peak); reorder-quantize HBM GB/s"
+UNIT = "TFLOP/s"
+
+CONFIGS = {
+    # name: (M, K, N, workload text)
+    "q_proj": (2048, 4096, 4096, "Llama-3.1-8B q_proj M=2048 K=4096 N=4096, calibrated thresholds"),
+    "llama70b_down": (8192, 28672, 8192,
+                      "Llama-3.1-70B down_proj M=8192 K=28672 N=8192, calibrated, N-sharded + BF16 all-gather"),
+    "cfg1": (16, 256, 256, "single linear M=16 K=256 N=256, fixed split 128/64/64, 4 outlier channels"),
+}
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written), else the
+    fallback in B200_PROFILING.md.  FP8/FP6 and FP4 dense peaks are the measured
+    bf16 peak x the nominal ratios 2x and 4x (2.25 -> 4.5 -> 9 PF)."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    src = "measured"
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        hbm, bf16 = float(p["hbm_gbs"]), float(p["bf16_tflops"])
+        bf16_s = float(p.get("bf16_tflops_sustained", bf16))
+    except Exception:
+        hbm, bf16, bf16_s, src = 6650.0, 1590.0, 1400.0, "fallback"
+    return dict(hbm_gbs=hbm, bf16=bf16, bf16_sustained=bf16_s, fp8=2 * bf16, fp4=4 * bf16, src=src)
+
+
+def mix_peak_tflops(n, pk):
+    """P_mix = K / (n4/P_FP4 + (n6+n8)/P_FP8) (FP6 runs at the FP8 rate)."""
+    K = sum(n)
+    return K / (n[0] / pk["fp4"] + (n[1] + n[2]) / pk["fp8"])
+
+
+def rq_bytes(M, n):
+    """Algorithmic reorder-quantize bytes: BF16 read + packed codes + E8M0 scales (no padding)."""
+    K = sum(n)
+    return 2 * M * K + M * (n[0] // 2 + 3 * n[1] // 4 + n[2]) + M * K // 32
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms in the background."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) arm
+def oracle_cpu_rate(M, K, N, budget_s=15.0, seed_layer=0):
+    """Time the CPU oracle (as it stands) on a bounded row sample of the workload:
+    reorder-quantize of the sampled activation rows + fp64 GEMM of the dequantized
+    operands against all N output channels.  The weight quantization is offline for
+    both arms and is done before timing.  Returns (TFLOP/s, sample text, threads, rows/s)."""
+    from oracle import calib as ocal
+    from oracle import mx as omx
+    from synth import bf16_bits, gen_act, gen_weight
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count()
+    cal = ocal.calibrate(bf16_bits(gen_act(2048 if K <= 8192 else 512, K, 1000 + seed_layer, 2000)))
+    perm, n = cal["perm"], cal["n"]
+    w_bits = bf16_bits(gen_weight(N, K, 3000 + seed_layer))
+    wc, wsf, _ = omx.reorder_quantize(w_bits, perm, n)
+    Wd = omx.dequantize_segments(wc, wsf)
+    # calibrate the sample size with a small probe, then run ~budget_s of work
+    rows = 8
+    total_rows, t_total = 0, 0.0
+    while t_total < budget_s:
+        x_bits = bf16_bits(gen_act(rows, K, 1000 + seed_layer, 5000 + total_rows))
+        t0 = time.perf_counter()
+        ac, asf, _ = omx.reorder_quantize(x_bits, perm, n)
+        y = omx.dequantize_segments(ac, asf) @ Wd.T
+        _ = omx.bf16_rne(y)
+        dt = time.perf_counter() - t0
+        total_rows += rows
+        t_total += dt
+        if total_rows >= M:
+            break
+        rows = max(8, min(M - total_rows, int(rows * max(1.0, min(4.0, (budget_s - t_total) / max(dt, 1e-3) / 2)))))
+    tflops = 2.0 * total_rows * N * K / t_total / 1e12
+    sample = (f"{total_rows} of {M} activation rows (reorder-quantize + fp64 GEMM vs all {N} channels), "
+              f"{t_total:.1f} s; weights quantized offline (untimed)")
+    return tflops, sample, threads, total_rows / t_total
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    M, K, N, text = CONFIGS[args.config]
+    vals = []
+    sample = ""
+    threads = 1
+    per = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    for i in range(args.warmup + args.steps):
+        v, sample, threads, _ = oracle_cpu_rate(M, K, N, budget_s=per)
+        if i >= args.warmup:
+            vals.append(v)
+    v = statistics.median(vals)
+    ms = 2.0 * M * N * K / (v * 1e12) * 1e3
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": text, "M": M, "K": K, "N": N},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def build_layer(M, K, N, n_sets, device, layer=0, calib_rows=16384, n_shard=None, rank=0, world=1):
+    """Offline part (untimed): calibrate on a calibration draw, quantize n_sets
+    distinct weight matrices, allocate n_sets activation / output buffers."""
+    import paper_2508_02343_b200 as mm
+    from synth import gen_act, gen_weight
+    cal_x = gen_act(calib_rows, K, 1000 + layer, 2000 + 10 * layer, device=device)
+    plan = mm.mm_calibrate_thresholds(cal_x)
+    del cal_x
+    Ns = N if n_shard is None else N // world
+    sets = []
+    for i in range(n_sets):
+        x = gen_act(M, K, 1000 + layer, 2001 + 10 * layer + 100 * i, device=device)
+        w = gen_weight(N, K, 3000 + layer + 100 * i, device=device)
+        if n_shard is not None:
+            w = w[rank * Ns:(rank + 1) * Ns].contiguous()
+        wq = mm.mm_quantize_weight_offline(w, plan)
+        del w
+        a = mm.MXTensor(plan, M, device)
+        y = torch.empty(M, N if n_shard is not None else Ns, dtype=torch.bfloat16, device=device)
+        sets.append(dict(x=x, wq=wq, a=a, y=y))
+    torch.cuda.synchronize()
+    return plan, sets
+
+
+def run_gpu(args, rank, world, local):
+    import paper_2508_02343_b200 as mm
+    M, K, N, text = CONFIGS[args.config]
+    dev = torch.device("cuda", local)
+    pk = peaks()
+    nshard = args.config == "llama70b_down" and world > 1
+    comm = None
+    if nshard:
+        import torch.distributed as dist
+        uid = [mm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = mm.mm_comm_init(rank, world, uid[0])
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    # bytes touched per step (for the L2 rotation count)
+    per_set = 2 * M * K + M * K + (N // world if nshard else N) * K + 2 * M * N
+    n_sets = max(2, min(16, -(-3 * l2 // per_set)))
+    if args.config == "cfg1":
+        n_sets = 2
+    plan, sets = build_layer(M, K, N, n_sets, dev, n_shard=(True if nshard else None), rank=rank, world=world,
+                             calib_rows=16384 if K <= 8192 else 2048)
+    n = plan.n
+    stage = torch.empty(M * N, dtype=torch.bfloat16, device=dev) if nshard else None
+    stream = torch.cuda.Stream(dev)
+    Ns = N // world if nshard else N
+
+    def step(i, evs=None):
+        s = sets[i % n_sets]
+        if evs is not None:
+            evs[0].record(stream)
+        mm.mm_reorder_quantize_act(s["x"], plan, out=s["a"], stream=stream)
+        if evs is not None:
+            evs[1].record(stream)
+        if nshard:
+            mm.mm_mixed_gemm_bf16_nshard_allgather(s["a"], s["wq"], plan, N, comm, out=s["y"], stage=stage,
+                                                   stream=stream)
+        else:
+            mm.mm_mixed_gemm_bf16(s["a"], s["wq"], plan, out=s["y"], stream=stream)
+        if evs is not None:
+            evs[2].record(stream)
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+        # keep the clocks honest: ~0.3 s of identical steps just before the timed region,
+        # sampled together with it
+        sampler = ClockSampler(local)
+        sampler.start()
+        t_end = time.time() + 0.3
+        i = 0
+        while time.time() < t_end:
+            step(i)
+            i += 1
+            if i % 64 == 0:
+                stream.synchronize()
+        stream.synchronize()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        torch.cuda.synchronize()
+        l0 = mm.launch_count()
+        t0.record(stream)
+        for i in range(args.steps):
+            step(i, evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        launches = mm.launch_count() - l0
+        clocks = sampler.stop()
+    total_ms = max_over_ranks(t0.elapsed_time(t1), world)
+    rq_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    gemm_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    ms = total_ms / args.steps
+    flops_rank = 2.0 * M * Ns * K
+    units = flops_rank * world * args.steps                       # all ranks' useful FLOPs
+    value = units / (total_ms * 1e-3) / 1e12
+    gemm_tflops = flops_rank / (gemm_ms * 1e-3) / 1e12
+    pmix = mix_peak_tflops(n, pk)
+    rqb = rq_bytes(M, n)
+    rq_gbs = rqb / (rq_ms * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers --------------------------
+    x_host = sets[0]["x"].cpu().pin_memory()
+    y_host = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+    x_dev, y_dev = sets[0]["x"], sets[0]["y"]
+    with torch.cuda.stream(stream):
+        def e2e_step():
+            x_dev.copy_(x_host, non_blocking=True)
+            mm.mm_reorder_quantize_act(x_dev, plan, out=sets[0]["a"], stream=stream)
+            if nshard:
+                mm.mm_mixed_gemm_bf16_nshard_allgather(sets[0]["a"], sets[0]["wq"], plan, N, comm, out=y_dev,
+                                                       stage=stage, stream=stream)
+            else:
+                mm.mm_mixed_gemm_bf16(sets[0]["a"], sets[0]["wq"], plan, out=y_dev, stream=stream)
+            y_host.copy_(y_dev, non_blocking=True)
+        for _ in range(max(3, args.warmup)):
+            e2e_step()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    e2e_val = units / (e2e_ms * 1e-3) / 1e12
+
+    if rank != 0:
+        return
+    # ---- CPU baseline (oracle as it stands, bounded sample) -----------------------------
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, sample, threads, _ = oracle_cpu_rate(M, K, N, budget_s=args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if nshard else "weak", "vs_baseline": None,
+        "dtype": "mxfp4/mxfp6(e3m2)/mxfp8(e4m3) x e8m0, fp32 accum, bf16 out", "data": "synthetic",
+        "config": {"workload": text, "M": M, "K": K, "N": N, "n4_n6_n8": list(n),
+                   "parallelism": (f"N-shard x{world} + NCCL all-gather" if nshard else
+                                   ("replicas" if world > 1 else "1 GPU")),
+                   "l2": f"{n_sets} rotating input/weight/output sets, {n_sets * per_set / 1e6:.0f} MB > L2 "
+                         f"{l2 / 1e6:.0f} MB"},
+        "breakdown": {"rq_us": rq_ms * 1e3, "gemm_us": gemm_ms * 1e3,
+                      "rq_gbs": rq_gbs, "rq_frac_hbm": rq_gbs / pk["hbm_gbs"],
+                      "gemm_tflops": gemm_tflops, "gemm_mix_peak_tflops": pmix,
+                      "gemm_frac_mix_peak": gemm_tflops / pmix,
+                      "peaks": f"{pk['src']}: HBM {pk['hbm_gbs']:.0f} GB/s, bf16 {pk['bf16']:.0f} TF/s "
+                               f"(fp8 = 2x, fp4 = 4x)"},
+        "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": pmix, "unit": "TFLOP/s",
+                     "frac": gemm_tflops / pmix, "traffic": None,
+                     "kernel": "mixgemm_kernel (algorithmic 2*M*N*K per launch; mix-weighted MXFP4/FP8 peak)"},
+        "rq_roofline": {"bound": "hbm", "achieved": rq_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": rq_gbs / pk["hbm_gbs"], "traffic": None,
+                        "kernel": "rq_kernel (algorithmic BF16 read + packed codes + scales)"},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 2 * M * K,
+                "d2h_bytes_per_step": 2 * M * N},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    if args.traffic:
+        try:
+            with open(os.path.join(ROOT, args.traffic)) as f:
+                tr = json.load(f)
+            out["roofline"]["traffic"] = tr.get("mixgemm")
+            out["rq_roofline"]["traffic"] = tr.get("rq")
+        except Exception:
+            pass
+    print(json.dumps(out), flush=True)
+    if comm is not None:
+        mm.mm_comm_destroy(comm)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="micromix", choices=["micromix", "reference"])
+    ap.add_argument("--config", default="q_proj", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", default="profiles/traffic_r01.json",
+                    help="ncu dram bytes per launch (written from an ncu --set full capture)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, rank, world)
+        return
+    rank, world, local = dist_init()
+    run_gpu(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
