@@ -150,12 +150,8 @@ def barrier(world):
 
 
 def max_over_ranks(v: float, world: int) -> float:
-    if world == 1:
-        return v
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2508_02343_b200.dist import max_over_ranks as mor
+    return mor(v, device="cuda") if world > 1 else v
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) arm
@@ -254,10 +250,8 @@ def run_gpu(args, rank, world, local):
     nshard = args.config == "llama70b_down" and world > 1
     comm = None
     if nshard:
-        import torch.distributed as dist
-        uid = [mm.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = mm.mm_comm_init(rank, world, uid[0])
+        from paper_2508_02343_b200.dist import exchange_unique_id
+        comm = mm.mm_comm_init(rank, world, exchange_unique_id(mm.nccl_unique_id))
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     # bytes touched per step (for the L2 rotation count)
     per_set = 2 * M * K + M * K + (N // world if nshard else N) * K + 2 * M * N

@@ -297,7 +297,5 @@ def mm_mixed_gemm_bf16_nshard_allgather(a: MXTensor, w_shard: MXTensor, plan: Pl
 
 def shard_rows(N: int, world: int, rank: int):
     """Rows of W owned by `rank` under N-sharding (host logic, CPU-testable)."""
-    if N % world:
-        raise ValueError("N must divide evenly across ranks")
-    ns = N // world
-    return rank * ns, (rank + 1) * ns
+    from .dist import shard_rows as _sr
+    return _sr(N, world, rank)

@@ -153,10 +153,13 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
         const int m0 = mb * BM, n0 = nb * BN;
         for (int s = 0; s < nstages; ++s) {
           const StageInfo si = stage_info(p, s);
-          ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1);
+          ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1, 1, s, t);
           const uint32_t fb = ptx::smem_u32(&full[stage]);
           const int kp128 = p.kp[si.g] / 128;
-          uint32_t bytes = C::A_BYTES + C::B_BYTES + si.atoms * 512;
+          // TMA counts transaction bytes in GLOBAL element bits: a 16U6 (FP6) box of
+          // 128 elements x rows lands as 128 B per smem row but completes 96 B per row.
+          uint32_t bytes = (si.g == 1 ? (C::A_BYTES + C::B_BYTES) / 4 * 3 : C::A_BYTES + C::B_BYTES) +
+                           si.atoms * 512;
           int nrg = 0;
 #pragma unroll
           for (int rg = 0; rg < C::RG; ++rg)
@@ -187,12 +190,12 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int acc = it % C::NUM_ACC;
       const uint32_t acc_phase = (it / C::NUM_ACC) & 1;
-      ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1);
+      ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1, 2, it, t);
       ptx::tc_fence_after();
       const uint32_t d_t = tmem_base + acc * BN;
       for (int s = 0; s < nstages; ++s) {
         const StageInfo si = stage_info(p, s);
-        ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase);
+        ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase, 3, s, t);
         ptx::tc_fence_after();
         if (lane == 0) {
           // scale atoms -> TMEM (32 rows x 16 B each, replicated to 4 lane quadrants)
@@ -234,7 +237,7 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
       const int mb = t % p.num_m, nb = t / p.num_m;
       const int acc = it % C::NUM_ACC;
       const uint32_t acc_phase = (it / C::NUM_ACC) & 1;
-      ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase);
+      ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase, 4, it, t);
       ptx::tc_fence_after();
       const int64_t row = (int64_t)mb * BM + q * 32 + lane;
       const int64_t n0 = (int64_t)nb * BN;

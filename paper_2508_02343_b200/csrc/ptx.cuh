@@ -1,6 +1,7 @@
 // ptx.cuh -- thin inline-PTX wrappers for sm_100a (mbarrier, TMA, tcgen05).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 namespace mmx {
 namespace ptx {
@@ -34,9 +35,34 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait for the phase with parity `parity` to complete.  Watchdog: a wait that
+// lasts longer than MM_WATCHDOG_NS (default 4 s; 0 disables) prints the site
+// and traps, so a pipeline bug surfaces as a launch error instead of a hang.
+#ifndef MM_WATCHDOG_NS
+#define MM_WATCHDOG_NS 4000000000ull
+#endif
+__device__ __noinline__ void watchdog_fire(int tag, uint32_t bar, uint32_t parity, int a, int b) {
+  printf("[mm watchdog] block %d thread %d: mbarrier wait tag=%d bar=0x%x parity=%u info=(%d,%d) timed out\n",
+         blockIdx.x, threadIdx.x, tag, bar, parity, a, b);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag = 0, int a = 0, int b = 0) {
+  if (mbar_try_wait(bar, parity)) return;
+#if MM_WATCHDOG_NS
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > (uint64_t)MM_WATCHDOG_NS) watchdog_fire(tag, bar, parity, a, b);
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // ---- TMA / bulk copies ---------------------------------------------------------
