@@ -246,6 +246,8 @@ def run_gpu(args, rank, world, local):
     import paper_2508_02343_b200 as mm
     M, K, N, text = CONFIGS[args.config]
     dev = torch.device("cuda", local)
+    if args.gemm_bn or args.gemm_stages:
+        mm.mm_set_gemm_config(args.gemm_bn, args.gemm_stages, 0)
     pk = peaks()
     nshard = args.config == "llama70b_down" and world > 1
     comm = None
@@ -406,6 +408,8 @@ def main():
     ap.add_argument("--config", default="q_proj", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gemm-bn", type=int, default=0, help="GEMM tile N override (tuning)")
+    ap.add_argument("--gemm-stages", type=int, default=0, help="GEMM pipeline stages override (tuning)")
     ap.add_argument("--traffic", default="profiles/traffic_r01.json",
                     help="ncu dram bytes per launch (written from an ncu --set full capture)")
     args = ap.parse_args()

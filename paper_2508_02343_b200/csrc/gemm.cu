@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -49,19 +50,24 @@ struct GemmDev {
   uint32_t idesc[3];     // instruction descriptors (sf ids = 0)
   uint16_t* y;
   int64_t ldy;
+  int dbg;               // timing experiments only (env MM_GEMM_DEBUG): 1 = SF copy once per tile, 2 = no MMA
 };
 
-template <int BN>
+template <int BN, int STAGES>
 struct Cfg {
   static constexpr int A_BYTES = BM * ROW_BYTES;
   static constexpr int B_BYTES = BN * ROW_BYTES;
   static constexpr int RG = BN / 128;               // 128-row scale groups of W per tile
   static constexpr int SFA_BYTES = 2 * 512;
   static constexpr int SFB_BYTES = 2 * RG * 512;
-  static constexpr int SF_COLS = 8 + 8 * RG;
-  static constexpr int NUM_ACC = (2 * BN + SF_COLS <= 512) ? 2 : 1;
-  static constexpr int SFA_COL = NUM_ACC * BN;
-  static constexpr int SFB_COL = SFA_COL + 8;
+  // TMEM columns: [accumulator(s) | one scale-factor slot per smem stage].  A slot
+  // holds up to 2 atoms of SFA (4 columns each) and 2 x RG atoms of SFB.  Giving
+  // every pipeline stage its own slot removes the write-after-read hazard between
+  // stage i's MMAs and stage i+1's tcgen05.cp, so the tensor pipe never drains.
+  static constexpr int SF_STRIDE = 8 + 8 * RG;
+  static constexpr int NUM_ACC = (2 * BN + STAGES * SF_STRIDE <= 512) ? 2 : 1;
+  static constexpr int SF_BASE = NUM_ACC * BN;
+  static_assert(NUM_ACC * BN + STAGES * SF_STRIDE <= 512, "TMEM budget");
 };
 
 struct StageInfo {
@@ -101,7 +107,7 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
                const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb0,
                const __grid_constant__ CUtensorMap tb1, const __grid_constant__ CUtensorMap tb2,
                const GemmDev p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -185,8 +191,6 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    const uint32_t sfa_t = tmem_base + C::SFA_COL;
-    const uint32_t sfb_t = tmem_base + C::SFB_COL;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int acc = it % C::NUM_ACC;
       const uint32_t acc_phase = (it / C::NUM_ACC) & 1;
@@ -198,8 +202,10 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
         ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase, 3, s, t);
         ptx::tc_fence_after();
         if (lane == 0) {
+          const uint32_t sfa_t = tmem_base + C::SF_BASE + stage * C::SF_STRIDE;
+          const uint32_t sfb_t = sfa_t + 8;
           // scale atoms -> TMEM (32 rows x 16 B each, replicated to 4 lane quadrants)
-          for (int at = 0; at < si.atoms; ++at) {
+          for (int at = 0; at < si.atoms && !((p.dbg & 1) && s > 0); ++at) {
             ptx::tc_cp_32x128b_x4(sfa_t + 4 * at,
                                   ptx::smem_desc(ptx::smem_u32(sSFA + stage * C::SFA_BYTES + at * 512), 0, 128, 0));
 #pragma unroll
@@ -210,7 +216,7 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
           }
           const uint32_t a_base = ptx::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_base = ptx::smem_u32(sB + stage * C::B_BYTES);
-          for (int k = 0; k < si.nmma; ++k) {
+          for (int k = 0; k < ((p.dbg & 2) ? 0 : si.nmma); ++k) {
             const uint64_t ad = ptx::smem_desc(a_base + 32 * k, 16, 1024, 2);
             const uint64_t bd = ptx::smem_desc(b_base + 32 * k, 16, 1024, 2);
             const uint32_t accum = (s > 0 || k > 0) ? 1u : 0u;
@@ -328,7 +334,7 @@ uint32_t make_idesc(int fmt, int g, int n) {
 
 template <int BN, int STAGES>
 size_t smem_bytes() {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, STAGES>;
   return 1024 + (size_t)STAGES * (C::A_BYTES + C::B_BYTES + C::SFA_BYTES + C::SFB_BYTES) +
          (2 * STAGES + 2 * C::NUM_ACC) * 8 + 16;
 }
@@ -370,6 +376,7 @@ cudaError_t run(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_
   p.sfb_rows_pad = (a.N + 127) / 128 * 128;
   p.y = a.y;
   p.ldy = a.ldy;
+  { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   if (p.num_tiles == 0) return cudaSuccess;
   const size_t smem = smem_bytes<BN, STAGES>();
   auto kern = mixgemm_kernel<BN, STAGES>;
