@@ -279,28 +279,11 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------- host
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn get_encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, []() {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(ptr);
-  });
-  return fn;
-}
-
 // 2-D K-major operand map: inner dim = K coordinate (bytes, or FP6 elements),
 // outer = rows; box = 128 x box_rows; 128-byte swizzle.
 bool make_operand_map(CUtensorMap* m, const void* base, int g, int kp, int64_t rows, int64_t pitch,
                       int box_rows) {
-  EncodeTiledFn enc = get_encode_fn();
+  EncodeTiledFn enc = tensor_map_encoder();
   if (!enc) return false;
   CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_UINT8;
   cuuint64_t inner;
@@ -380,7 +363,7 @@ cudaError_t run(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_
   if (p.num_tiles == 0) return cudaSuccess;
   const size_t smem = smem_bytes<BN, STAGES>();
   auto kern = mixgemm_kernel<BN, STAGES>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
   int grid = sm_count();
   if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas;
@@ -391,6 +374,19 @@ cudaError_t run(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_
 }
 
 }  // namespace
+
+EncodeTiledFn tensor_map_encoder() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
 
 cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
                               const char** err) {

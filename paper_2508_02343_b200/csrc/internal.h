@@ -1,6 +1,7 @@
 // internal.h -- launch interfaces between the C-ABI layer (mm_api.cpp) and the
 // sm_100a kernels.  Not part of the public ABI (that is include/mm.h).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <cstdint>
@@ -69,6 +70,19 @@ cudaError_t launch_gather_layout(const uint16_t* stage, int G, int64_t M, int64_
                                  uint16_t* y, int64_t ldy, cudaStream_t s, int64_t* launches);
 
 int sm_count();
+
+// cuTensorMapEncodeTiled resolved through the runtime (no libcuda link); nullptr if
+// the driver does not provide it (gemm.cu).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn tensor_map_encoder();
+
+// Host-side launch caches (per device, thread-safe): raise a kernel's dynamic
+// shared-memory limit once, and remember occupancy queries, so the hot calls do
+// no redundant driver work per launch.
+cudaError_t ensure_smem_attr(const void* func, size_t smem);
+cudaError_t cached_occupancy(const void* func, int threads, size_t smem, int* per_sm);
 
 // NCCL entry points resolved with dlopen (comm.cu).
 struct NcclApi {

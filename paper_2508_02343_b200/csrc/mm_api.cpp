@@ -11,7 +11,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -145,7 +147,7 @@ uint64_t fingerprint(int32_t K, const int32_t n[3], int32_t fmt6, int32_t fmt8, 
 }
 
 // Shared memory the reorder-quantize kernel needs for this K (R = 1 layout).
-bool rq_fits(int32_t K) { return (size_t)K * 2 * 3 + 256 <= 220 * 1024; }
+bool rq_fits(int32_t K) { return (size_t)((K + 255) / 256) * 512 * 2 <= 200 * 1024; }   // >= 2 one-row stages
 
 mm_status check_mx_out(const mm_plan* p, const mm_mx_tensor* t, int64_t rows, const char* what) {
   if (!t) return fail(MM_ERR_INVALID_ARGUMENT, "%s is NULL", what);
@@ -202,6 +204,35 @@ int sm_count() {
     cached[dev] = v > 0 ? v : 1;
   }
   return cached[dev];
+}
+
+namespace {
+std::mutex g_cache_mu;
+std::map<std::pair<const void*, int>, size_t> g_smem_attr;
+std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;
+}  // namespace
+
+cudaError_t ensure_smem_attr(const void* func, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  size_t& cur = g_smem_attr[{func, dev}];
+  if (smem <= cur) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
+
+cudaError_t cached_occupancy(const void* func, int threads, size_t smem, int* per_sm) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto key = std::make_tuple(func, dev, threads, smem);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) { *per_sm = it->second; return cudaSuccess; }
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, func, threads, smem);
+  if (e == cudaSuccess) g_occ[key] = *per_sm;
+  return e;
 }
 
 }  // namespace mmx

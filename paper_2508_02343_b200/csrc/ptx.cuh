@@ -46,7 +46,7 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 #ifndef MM_WATCHDOG_NS
 #define MM_WATCHDOG_NS 4000000000ull
 #endif
-__device__ __noinline__ void watchdog_fire(int tag, uint32_t bar, uint32_t parity, int a, int b) {
+static __device__ __noinline__ void watchdog_fire(int tag, uint32_t bar, uint32_t parity, int a, int b) {
   printf("[mm watchdog] block %d thread %d: mbarrier wait tag=%d bar=0x%x parity=%u info=(%d,%d) timed out\n",
          blockIdx.x, threadIdx.x, tag, bar, parity, a, b);
   __trap();
@@ -65,6 +65,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag
 #endif
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // ---- TMA / bulk copies ---------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
@@ -75,6 +79,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* desc, uint
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* desc, uint32_t bar, int32_t c0,
+                                            int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {

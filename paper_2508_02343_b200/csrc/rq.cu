@@ -2,16 +2,15 @@
 // channel segments (§3.2 "Quantization Kernel", line 151; Fig. 6
 // caption line 148; Eq. 1 lines 40-45), sm_100a.
 //
-// HBM-bound streaming kernel.  Persistent CTAs, warp-specialised:
-//   * 4 producer warps stream R rows at a time from HBM with 128-bit loads and
-//     write them into shared memory "row-interleaved": smem slot p holds the R
-//     BF16 values of channel p (R = 4: 8-byte slots), XOR-swizzled so the
-//     128-bit -> slot transposition stores are bank-conflict free.  Two slots
-//     (double buffer) overlap the next tile's loads with this tile's work.
-//   * 4 consumer warps own one 32-channel block of the reordered row each:
-//     the gather x_r[j] = X[perm[j]] is a single 64-bit shared load per channel
-//     that fetches all R rows at once (R-fold fewer random smem accesses than a
-//     per-row gather); block amax is an integer max over |bf16| bits; the E8M0
+// HBM-bound streaming kernel (see rq_kernel below for the tile structure):
+//   * R rows at a time are streamed from HBM with 128-bit loads and written into
+//     shared memory "row-interleaved": smem slot p holds the R BF16 values of
+//     channel p (R = 2: 4-byte slots), XOR-swizzled so the 128-bit -> slot
+//     transposition stores are bank-conflict free;
+//   * a thread owns one 32-channel block of the reordered row: the gather
+//     x_r[j] = X[perm[j]] is a single shared load per channel that fetches all R
+//     rows at once (R-fold fewer random smem accesses than a per-row gather);
+//     block amax is an integer max over |bf16| bits; the E8M0
 //     exponent is integer arithmetic on the BF16 exponent field (no log2f); the
 //     scaled value x * 2^-e is exact (power of two, no FTZ); the element code is
 //     produced by the hardware cvt.rn.satfinite.{e2m1x2,e3m2x2,e2m3x2,e4m3x2,
@@ -23,72 +22,77 @@
 //   multiple of 128 are written as zero on every call.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace mmx {
 namespace {
 
-constexpr int kProdThreads = 128;
-constexpr int kConsThreads = 128;
-constexpr int kThreads = kProdThreads + kConsThreads;
 
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void named_bar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// Slot swizzle: slot(p) = p ^ ((p >> S) & (W - 1)) with W slots per 128-byte line.
-template <int R> struct SlotT;
-template <> struct SlotT<1> { using T = uint16_t; static constexpr int W = 1, S = 0; };
-template <> struct SlotT<2> { using T = uint32_t; static constexpr int W = 32, S = 5; };
-template <> struct SlotT<4> { using T = uint2; static constexpr int W = 16, S = 4; };
-
-template <int R>
-__device__ __forceinline__ uint32_t swz(uint32_t p) {
-  if constexpr (R == 1) return p;
-  else return p ^ ((p >> SlotT<R>::S) & (SlotT<R>::W - 1));
-}
-
-template <int R>
-__device__ __forceinline__ uint32_t row_bits(const typename SlotT<R>::T& v, int rho) {
-  if constexpr (R == 1) return v;
-  else if constexpr (R == 2) return (v >> (16 * rho)) & 0xFFFFu;
-  else return ((rho < 2 ? v.x : v.y) >> (16 * (rho & 1))) & 0xFFFFu;
-}
-
-// ---- element conversions (hardware RNE + satfinite) -------------------------
+// ---- element conversions (hardware RNE + satfinite, sign-preserving) --------
 // cvt.*x2.f32 d, a, b puts a in the upper half of d and b in the lower half.
-__device__ __forceinline__ uint32_t cvt_fp8x2(float lo, float hi, int fmt) {
-  uint16_t r;
-  if (fmt == F_E4M3)
-    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
-  else
-    asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
-  return r;
+template <int FMT> struct Cvt;
+template <> struct Cvt<F_E4M3> {
+  static __device__ __forceinline__ uint32_t x4(float a0, float a1, float a2, float a3) {
+    uint32_t r;
+    asm("{\n\t.reg .b16 h0, h1;\n\t"
+        "cvt.rn.satfinite.e4m3x2.f32 h0, %2, %1;\n\t"
+        "cvt.rn.satfinite.e4m3x2.f32 h1, %4, %3;\n\t"
+        "mov.b32 %0, {h0, h1};\n\t}" : "=r"(r) : "f"(a0), "f"(a1), "f"(a2), "f"(a3));
+    return r;
+  }
+};
+template <> struct Cvt<F_E5M2> {
+  static __device__ __forceinline__ uint32_t x4(float a0, float a1, float a2, float a3) {
+    uint32_t r;
+    asm("{\n\t.reg .b16 h0, h1;\n\t"
+        "cvt.rn.satfinite.e5m2x2.f32 h0, %2, %1;\n\t"
+        "cvt.rn.satfinite.e5m2x2.f32 h1, %4, %3;\n\t"
+        "mov.b32 %0, {h0, h1};\n\t}" : "=r"(r) : "f"(a0), "f"(a1), "f"(a2), "f"(a3));
+    return r;
+  }
+};
+// FP6: four codes -> 24-bit LSB-first stream c0 | c1<<6 | c2<<12 | c3<<18, from
+// t = c0 | c1<<8 | c2<<16 | c3<<24 (each code 6 bits): close the byte gaps pairwise.
+__device__ __forceinline__ uint32_t pack6(uint32_t t) {
+  const uint32_t w = (t & 0x003F003Fu) | ((t >> 2) & 0x0FC00FC0u);   // c0|c1<<6 , c2|c3<<6 at bit 16
+  return (w & 0xFFFu) | ((w >> 4) & 0xFFF000u);
 }
-__device__ __forceinline__ uint32_t cvt_fp6x2(float lo, float hi, int fmt) {
-  uint16_t r;
-  if (fmt == F_E3M2)
-    asm("cvt.rn.satfinite.e3m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
-  else
-    asm("cvt.rn.satfinite.e2m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
-  return r;  // byte0 = code(lo) (6 bits), byte1 = code(hi)
-}
-// Four E2M1 codes -> one 16-bit value, element 0 in the lowest nibble.
-__device__ __forceinline__ uint32_t cvt_fp4x4(float a0, float a1, float a2, float a3) {
+template <> struct Cvt<F_E3M2> {
+  static __device__ __forceinline__ uint32_t x4(float a0, float a1, float a2, float a3) {
+    uint32_t t;
+    asm("{\n\t.reg .b16 h0, h1;\n\t"
+        "cvt.rn.satfinite.e3m2x2.f32 h0, %2, %1;\n\t"
+        "cvt.rn.satfinite.e3m2x2.f32 h1, %4, %3;\n\t"
+        "mov.b32 %0, {h0, h1};\n\t}" : "=r"(t) : "f"(a0), "f"(a1), "f"(a2), "f"(a3));
+    return pack6(t);
+  }
+};
+template <> struct Cvt<F_E2M3> {
+  static __device__ __forceinline__ uint32_t x4(float a0, float a1, float a2, float a3) {
+    uint32_t t;
+    asm("{\n\t.reg .b16 h0, h1;\n\t"
+        "cvt.rn.satfinite.e2m3x2.f32 h0, %2, %1;\n\t"
+        "cvt.rn.satfinite.e2m3x2.f32 h1, %4, %3;\n\t"
+        "mov.b32 %0, {h0, h1};\n\t}" : "=r"(t) : "f"(a0), "f"(a1), "f"(a2), "f"(a3));
+    return pack6(t);
+  }
+};
+// FP4: eight codes -> one 32-bit word, element 0 in the lowest nibble.
+__device__ __forceinline__ uint32_t cvt_e2m1_x8(const float (&f)[8]) {
   uint32_t r;
-  asm("{\n\t.reg .b8 b0, b1;\n\t"
+  asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\t"
       "cvt.rn.satfinite.e2m1x2.f32 b0, %2, %1;\n\t"
       "cvt.rn.satfinite.e2m1x2.f32 b1, %4, %3;\n\t"
-      "mov.b32 %0, {b0, b1, 0, 0};\n\t}"
-      : "=r"(r) : "f"(a0), "f"(a1), "f"(a2), "f"(a3));
+      "cvt.rn.satfinite.e2m1x2.f32 b2, %6, %5;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b3, %8, %7;\n\t"
+      "mov.b32 %0, {b0, b1, b2, b3};\n\t}"
+      : "=r"(r)
+      : "f"(f[0]), "f"(f[1]), "f"(f[2]), "f"(f[3]), "f"(f[4]), "f"(f[5]), "f"(f[6]), "f"(f[7]));
   return r;
 }
-
-__device__ __forceinline__ float bf16_to_f32(uint32_t b) { return __uint_as_float(b << 16); }
 
 // Byte offset of scale (r, kb) inside the 128x4-atom layout of a segment with
 // kp128 = Kp/128 atoms per 128-row group.
@@ -96,190 +100,343 @@ __device__ __forceinline__ int64_t sf_offset(int64_t r, int kb, int kp128) {
   return ((r >> 7) * kp128 + (kb >> 2)) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (kb & 3);
 }
 
-// Quantize one row's 32-element block `v` (BF16 bits) and store codes+scale.
-__device__ __forceinline__ void quantize_store_block(const uint32_t (&v)[32], int g, int fmt,
-                                                     int off, uint8_t* codes_row, int kb,
-                                                     bool store_codes, uint8_t* sf, int64_t r,
-                                                     int kp128) {
-  uint32_t amax = 0;
+// Slot types: the R BF16 values of one channel, rows interleaved (even rows in
+// the low halves): R = 1 -> uint16_t, 2 -> uint32_t, 4 -> uint2 {rows 0|1, 2|3}.
+template <int R> struct Slot;
+template <> struct Slot<1> { using T = uint16_t; };
+template <> struct Slot<2> { using T = uint32_t; };
+template <> struct Slot<4> { using T = uint2; };
+
+// Row RHO of a slot as an fp32 value (BF16 = the top half of an fp32).
+template <int RHO>
+__device__ __forceinline__ float slot_f32(const uint16_t& s) { return __uint_as_float(uint32_t(s) << 16); }
+template <int RHO>
+__device__ __forceinline__ float slot_f32(const uint32_t& s) {
+  return (RHO & 1) == 0 ? __uint_as_float(s << 16) : __uint_as_float(s & 0xFFFF0000u);
+}
+template <int RHO>
+__device__ __forceinline__ float slot_f32(const uint2& s) {
+  const uint32_t w = (RHO < 2) ? s.x : s.y;
+  return (RHO & 1) == 0 ? __uint_as_float(w << 16) : __uint_as_float(w & 0xFFFF0000u);
+}
+
+// Scale 8 consecutive elements of row RHO by 2^-e (exact; packed fp32x2 multiply).
+template <int RHO, typename ST>
+__device__ __forceinline__ void scaled8(const ST* v, float inv, float (&f)[8]) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) amax = max(amax, v[i] & 0x7FFFu);
-  // e = floor(log2 amax) - off, clamped at -127 (zero / subnormal blocks -> -127).
-  int sb = max(int(amax >> 7) - off, 0);          // E8M0 byte = e + 127
-  float inv = __uint_as_float(uint32_t(254 - sb) << 23);  // 2^-e exactly
-  sf[sf_offset(r, kb, kp128)] = uint8_t(sb);
-  if (!store_codes) return;
-  if (g == 0) {  // MXFP4: 16 bytes
-    uint32_t w[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t lo = cvt_fp4x4(bf16_to_f32(v[8 * q + 0]) * inv, bf16_to_f32(v[8 * q + 1]) * inv,
-                              bf16_to_f32(v[8 * q + 2]) * inv, bf16_to_f32(v[8 * q + 3]) * inv);
-      uint32_t hi = cvt_fp4x4(bf16_to_f32(v[8 * q + 4]) * inv, bf16_to_f32(v[8 * q + 5]) * inv,
-                              bf16_to_f32(v[8 * q + 6]) * inv, bf16_to_f32(v[8 * q + 7]) * inv);
-      w[q] = lo | (hi << 16);
-    }
-    *reinterpret_cast<uint4*>(codes_row + 16 * kb) = make_uint4(w[0], w[1], w[2], w[3]);
-  } else if (g == 1) {  // MXFP6: 24 bytes, LSB-first 6-bit stream
-    uint32_t q24[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      uint32_t h0 = cvt_fp6x2(bf16_to_f32(v[4 * q + 0]) * inv, bf16_to_f32(v[4 * q + 1]) * inv, fmt);
-      uint32_t h1 = cvt_fp6x2(bf16_to_f32(v[4 * q + 2]) * inv, bf16_to_f32(v[4 * q + 3]) * inv, fmt);
-      q24[q] = (h0 & 0x3Fu) | (((h0 >> 8) & 0x3Fu) << 6) | ((h1 & 0x3Fu) << 12) |
-               (((h1 >> 8) & 0x3Fu) << 18);
-    }
-    uint2* dst = reinterpret_cast<uint2*>(codes_row + 24 * kb);
-    dst[0] = make_uint2(q24[0] | (q24[1] << 24), (q24[1] >> 8) | (q24[2] << 16));
-    dst[1] = make_uint2((q24[2] >> 16) | (q24[3] << 8), q24[4] | (q24[5] << 24));
-    dst[2] = make_uint2((q24[5] >> 8) | (q24[6] << 16), (q24[6] >> 16) | (q24[7] << 8));
-  } else {  // MXFP8: 32 bytes
-    uint32_t w[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      uint32_t lo = cvt_fp8x2(bf16_to_f32(v[4 * q + 0]) * inv, bf16_to_f32(v[4 * q + 1]) * inv, fmt);
-      uint32_t hi = cvt_fp8x2(bf16_to_f32(v[4 * q + 2]) * inv, bf16_to_f32(v[4 * q + 3]) * inv, fmt);
-      w[q] = lo | (hi << 16);
-    }
-    uint4* dst = reinterpret_cast<uint4*>(codes_row + 32 * kb);
-    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  for (int i = 0; i < 8; i += 2) {
+    const float2 p = __fmul2_rn(make_float2(slot_f32<RHO>(v[i]), slot_f32<RHO>(v[i + 1])), make_float2(inv, inv));
+    f[i] = p.x;
+    f[i + 1] = p.y;
   }
 }
 
-template <int R>
-__global__ void __launch_bounds__(kThreads, 1)
-rq_kernel(const RqArgs a, int64_t rows_pad, int64_t n_tiles) {
-  using ST = typename SlotT<R>::T;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int K = a.K;
-  const int nblk = K / 32;                       // real blocks of the reordered row
-  // [gidx: u32 pairs, (K/2) words laid out [i/2][blk]] [slot0][slot1]
-  uint32_t* gidx2 = reinterpret_cast<uint32_t*>(smem);
-  const size_t gbytes = ((size_t)K * 2 + 127) / 128 * 128;
-  ST* buf0 = reinterpret_cast<ST*>(smem + gbytes);
-  ST* buf1 = buf0 + K;
+// Encode + store row RHO of one 32-element block (v = the 32 gathered two-row
+// slots) for segment kind G (0 FP4, 1 FP6, 2 FP8) in element format FMT.
+template <int G, int FMT, int RHO, typename ST>
+__device__ __forceinline__ void encode_store(const ST (&v)[32], float inv, uint8_t* dst) {
+  if constexpr (G == 0) {  // MXFP4: 16 bytes
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float f[8];
+      scaled8<RHO>(v + 8 * q, inv, f);
+      w[q] = cvt_e2m1_x8(f);
+    }
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else if constexpr (G == 1) {  // MXFP6: 24 bytes, LSB-first 6-bit stream
+    uint32_t q24[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float f[8];
+      scaled8<RHO>(v + 8 * q, inv, f);
+      q24[2 * q] = Cvt<FMT>::x4(f[0], f[1], f[2], f[3]);
+      q24[2 * q + 1] = Cvt<FMT>::x4(f[4], f[5], f[6], f[7]);
+    }
+    uint2* d2 = reinterpret_cast<uint2*>(dst);
+    d2[0] = make_uint2(q24[0] | (q24[1] << 24), (q24[1] >> 8) | (q24[2] << 16));
+    d2[1] = make_uint2((q24[2] >> 16) | (q24[3] << 8), q24[4] | (q24[5] << 24));
+    d2[2] = make_uint2((q24[5] >> 8) | (q24[6] << 16), (q24[6] >> 16) | (q24[7] << 8));
+  } else {  // MXFP8: 32 bytes
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float f[8];
+      scaled8<RHO>(v + 8 * q, inv, f);
+      w[2 * q] = Cvt<FMT>::x4(f[0], f[1], f[2], f[3]);
+      w[2 * q + 1] = Cvt<FMT>::x4(f[4], f[5], f[6], f[7]);
+    }
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+}
 
-  // Gather indices (swizzled smem slots) of reordered position j = 32*blk + i,
-  // stored transposed so that lanes (consecutive blk) read consecutive words.
-  for (int w = threadIdx.x; w < K / 2; w += blockDim.x) {
-    int i2 = w / nblk, blk = w % nblk;
-    int j = 32 * blk + 2 * i2;
-    uint32_t p0 = swz<R>(uint32_t(__ldg(a.perm + j)));
-    uint32_t p1 = swz<R>(uint32_t(__ldg(a.perm + j + 1)));
-    gidx2[w] = p0 | (p1 << 16);
+// Block amax of each of the R rows over |bf16| bits (packed 16x2 maxima).
+__device__ __forceinline__ void block_amax(const uint16_t (&v)[32], uint32_t (&am)[4]) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) m = max(m, uint32_t(v[i]) & 0x7FFFu);
+  am[0] = m;
+}
+__device__ __forceinline__ void block_amax(const uint32_t (&v)[32], uint32_t (&am)[4]) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) m = __vmaxu2(m, v[i] & 0x7FFF7FFFu);
+  am[0] = m & 0xFFFFu;
+  am[1] = m >> 16;
+}
+__device__ __forceinline__ void block_amax(const uint2 (&v)[32], uint32_t (&am)[4]) {
+  uint32_t m01 = 0, m23 = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    m01 = __vmaxu2(m01, v[i].x & 0x7FFF7FFFu);
+    m23 = __vmaxu2(m23, v[i].y & 0x7FFF7FFFu);
+  }
+  am[0] = m01 & 0xFFFFu;
+  am[1] = m01 >> 16;
+  am[2] = m23 & 0xFFFFu;
+  am[3] = m23 >> 16;
+}
+
+// One row of one block: E8M0 exponent by integer arithmetic on the BF16 exponent
+// field (e = floor(log2 amax) - off, clamped at -127; zero and subnormal amax give
+// -127), the scale byte into its 128x4 atom (rows of a tile are consecutive rows of
+// one 32-row group: +16 bytes per row), codes packed and stored.
+template <int RHO, int G, int FMT, typename ST>
+__device__ __forceinline__ void quantize_row(const ST (&v)[32], uint32_t amax, int off, uint8_t* crow,
+                                             uint8_t* sfp, bool store_codes) {
+  const int sb = max(int(amax >> 7) - off, 0);                  // E8M0 byte = e + 127
+  const float inv = __uint_as_float(uint32_t(254 - sb) << 23);  // 2^-e exactly
+  sfp[16 * RHO] = uint8_t(sb);
+  if (store_codes) encode_store<G, FMT, RHO>(v, inv, crow);
+}
+
+template <int R, int G, int FMT>
+__device__ __forceinline__ void quantize_tile_block(const typename Slot<R>::T (&v)[32], int off, uint8_t* crow0,
+                                                    int64_t pitch, uint8_t* sfp, int nvalid) {
+  uint32_t am[4];
+  block_amax(v, am);
+  quantize_row<0, G, FMT>(v, am[0], off, crow0, sfp, nvalid > 0);
+  if constexpr (R >= 2) quantize_row<1, G, FMT>(v, am[1], off, crow0 + pitch, sfp, nvalid > 1);
+  if constexpr (R >= 4) {
+    quantize_row<2, G, FMT>(v, am[2], off, crow0 + 2 * pitch, sfp, nvalid > 2);
+    quantize_row<3, G, FMT>(v, am[3], off, crow0 + 3 * pitch, sfp, nvalid > 3);
+  }
+}
+
+struct RqDev {
+  RqArgs a;
+  int64_t n_tiles;      // tiles of R rows covering roundup(rows, 128)
+  int nbox;             // TMA boxes of 256 channels per row
+  int stages, groups, group_warps;
+  int perm_smem;        // 1: permutation staged in smem as a gather table, 0: read through L1
+  int box3d;            // 1: one 3-D TMA per tile ({256, R, nbox} box), 0: nbox 2-D boxes
+  int dbg;              // timing experiments only (env MM_RQ_DEBUG): 1 = skip gather/quantize, 2 = skip transpose too
+};
+
+// Fused reorder-and-quantize, warp-specialised and TMA-fed:
+//  * warp 0 (one thread) streams tiles of R rows into a ring of `stages` shared
+//    memory buffers with 2-D TMA loads (boxes of 256 channels x R rows, one
+//    mbarrier per stage) -- HBM latency is hidden by the ring depth, not by
+//    registers;
+//  * `groups` consumer groups of `group_warps` warps take tiles round-robin.  For
+//    each tile a group first transposes the stage in place, warp w owning whole
+//    256-channel boxes, into "row-interleaved" slots (slot p = the R BF16 values
+//    of channel p at byte p * 2R); then thread t owns 32-channel blocks of the
+//    reordered rows: the gather x_r[j] = X[perm[j]] is one shared load per
+//    channel that returns all R rows (the permutation is read through L1 as
+//    16-byte vectors), block amax, scale and encode as above; finally the stage
+//    is released to the producer.
+template <int R>
+__global__ void __launch_bounds__(512, 1)
+rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev d) {
+  using ST = typename Slot<R>::T;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment by pointer arithmetic on the shared pointer (keeps the
+  // shared state space: a uintptr_t round trip would turn every access generic).
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const RqArgs& a = d.a;
+  const int stage_bytes = d.nbox * 512 * R;
+  // [ring of stages][perm copy: K x int32][gather table: K x u16][barriers]
+  const int K = a.K, nblk = K / 32;
+  const size_t tab_bytes = d.perm_smem ? (size_t)K * 6 : 0;
+  const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
+  uint32_t* gidx = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + (size_t)K * 4);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)d.stages * stage_bytes + tab_bytes);
+  uint64_t* empty = full + d.stages;
+  uint64_t* permbar = empty + d.stages;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < d.stages; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), d.group_warps);
+    }
+    ptx::mbar_init(ptx::smem_u32(permbar), 1);
+    ptx::fence_barrier_init();
+    ptx::tma_prefetch_desc(&tmx);
+    if (d.perm_smem) {  // the permutation arrives asynchronously, alongside the first tiles
+      ptx::mbar_arrive_expect_tx(ptx::smem_u32(permbar), (uint32_t)K * 4);
+      ptx::bulk_load(ptx::smem_u32(perm_s), a.perm, (uint32_t)K * 4, ptx::smem_u32(permbar));
+    }
   }
   __syncthreads();
+  const int64_t my_tiles = (d.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
-  const int64_t my_tiles = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  if (threadIdx.x < kProdThreads) {
-    // ---------------- producers: HBM -> row-interleaved smem ----------------
-    const int pt = threadIdx.x;
-    const int nchunk = K / 8;                      // 8 channels = 16 bytes per row
-    constexpr int U = 16 / R;                      // chunks in flight per thread
-    for (int64_t i = 0; i < my_tiles; ++i) {
-      const int slot = int(i & 1);
-      if (i >= 2) named_bar_sync(1 + 2 + slot, kThreads);      // EMPTY[slot]
-      ST* buf = slot ? buf1 : buf0;
-      const int64_t r0 = (blockIdx.x + i * gridDim.x) * R;
-      for (int c0 = pt; c0 < nchunk; c0 += kProdThreads * U) {
-        uint4 d[U][R];
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      const uint32_t tx = (uint32_t)stage_bytes;
+      for (int64_t i = 0; i < my_tiles; ++i) {
+        const int s = int(i % d.stages);
+        const uint32_t ph = uint32_t(i / d.stages) & 1u;
+        ptx::mbar_wait(ptx::smem_u32(&empty[s]), ph ^ 1u, 11, s, (int)i);
+        const uint32_t fb = ptx::smem_u32(&full[s]);
+        if (d.dbg & 4) { ptx::mbar_arrive(fb); continue; }   // timing experiment: no loads
+        ptx::mbar_arrive_expect_tx(fb, tx);
+        const int row0 = (int)((blockIdx.x + i * gridDim.x) * R);
+        const uint32_t dst = ptx::smem_u32(smem + (size_t)s * stage_bytes);
+        if (d.box3d) ptx::tma_load_3d(dst, &tmx, fb, 0, row0, 0);   // all boxes of the tile at once
+        else
+          for (int b = 0; b < d.nbox; ++b) ptx::tma_load_2d(dst + b * 512 * R, &tmx, fb, 256 * b, row0);
+      }
+    }
+    return;
+  }
+  // ============================ consumer groups ============================
+  const int cw = warp - 1;
+  const int grp = cw / d.group_warps, gw = cw % d.group_warps;
+  if (grp >= d.groups) return;
+  const int gthreads = d.group_warps * 32;
+  // Kernel parameters are copied into (uniform) registers once: indexing the
+  // parameter block inside the loop would go through generic/local memory.
+  const int stages = d.stages, groups = d.groups, group_warps = d.group_warps, nbox = d.nbox, dbg = d.dbg;
+  const int64_t rows = a.rows;
+  const int kp0 = a.geom.kp[0], kp1 = a.geom.kp[1], kp2 = a.geom.kp[2];
+  const int n0 = a.geom.n[0], n1 = a.geom.n[1], n2 = a.geom.n[2];
+  const int of0 = a.geom.off[0], of1 = a.geom.off[1], of2 = a.geom.off[2];
+  const int fm1 = a.geom.fmt[1], fm2 = a.geom.fmt[2];
+  const int so0 = a.geom.sc_off[0], so1 = a.geom.sc_off[1], so2 = a.geom.sc_off[2];
+  const int64_t pt0 = a.geom.pitch[0], pt1 = a.geom.pitch[1], pt2 = a.geom.pitch[2];
+  uint8_t* const cd0 = a.codes[0];
+  uint8_t* const cd1 = a.codes[1];
+  uint8_t* const cd2 = a.codes[2];
+  uint8_t* const sf0 = a.sf[0];
+  uint8_t* const sf1 = a.sf[1];
+  uint8_t* const sf2 = a.sf[2];
+  // Gather table: u16 channel indices, two per word, transposed [i/2][block] so
+  // the lanes of a warp (consecutive blocks) read consecutive words.
+  const bool use_tab = d.perm_smem != 0;
+  if (use_tab) {
+    ptx::mbar_wait(ptx::smem_u32(permbar), 0, 13, 0, 0);
+    const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
+    for (int t = ct; t < K / 2; t += cn) {
+      const int blk = t >> 4, i2 = t & 15;
+      const uint2 pr = *reinterpret_cast<const uint2*>(perm_s + 32 * blk + 2 * i2);
+      gidx[i2 * nblk + blk] = pr.x | (pr.y << 16);
+    }
+    ptx::named_bar_sync(15, cn);
+  }
+  // Work is split into chunks of 32 consecutive blocks of ONE segment (a warp's
+  // lanes never mix segments, so the encode path is warp-uniform).
+  const int nch0 = (kp0 / 32 + 31) / 32, nch1 = (kp1 / 32 + 31) / 32, nch2 = (kp2 / 32 + 31) / 32;
+  const int nch = nch0 + nch1 + nch2;
+  for (int64_t i = grp; i < my_tiles; i += groups) {
+    const int s = int(i % stages);
+    const uint32_t ph = uint32_t(i / stages) & 1u;
+    uint8_t* st = smem + (size_t)s * stage_bytes;
+    ptx::mbar_wait(ptx::smem_u32(&full[s]), ph, 12, s, (int)i);
+    // ---- in-place transpose: box [R rows][256] -> 256 slots of R values ----
+    if constexpr (R > 1) {
+      for (int b = gw; b < nbox && dbg < 2; b += group_warps) {
+        uint8_t* box = st + b * 512 * R;
+        uint4 w[R];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int c = c0 + u * kProdThreads;
+        for (int rho = 0; rho < R; ++rho) w[rho] = *reinterpret_cast<const uint4*>(box + rho * 512 + lane * 16);
+        __syncwarp();
+        const uint32_t* u0 = reinterpret_cast<const uint32_t*>(&w[0]);
+        const uint32_t* u1 = reinterpret_cast<const uint32_t*>(&w[1]);
+        if constexpr (R == 2) {
+          uint4* o = reinterpret_cast<uint4*>(box + lane * 32);
+          o[0] = make_uint4(__byte_perm(u0[0], u1[0], 0x5410), __byte_perm(u0[0], u1[0], 0x7632),
+                            __byte_perm(u0[1], u1[1], 0x5410), __byte_perm(u0[1], u1[1], 0x7632));
+          o[1] = make_uint4(__byte_perm(u0[2], u1[2], 0x5410), __byte_perm(u0[2], u1[2], 0x7632),
+                            __byte_perm(u0[3], u1[3], 0x5410), __byte_perm(u0[3], u1[3], 0x7632));
+        } else {
+          const uint32_t* u2 = reinterpret_cast<const uint32_t*>(&w[2]);
+          const uint32_t* u3 = reinterpret_cast<const uint32_t*>(&w[3]);
+          uint4* o = reinterpret_cast<uint4*>(box + lane * 64);
 #pragma unroll
-          for (int rho = 0; rho < R; ++rho) {
-            const int64_t r = r0 + rho;
-            if (c < nchunk && r < a.rows)
-              d[u][rho] = __ldcs(reinterpret_cast<const uint4*>(a.x + r * a.ldx) + c);
-            else
-              d[u][rho] = make_uint4(0, 0, 0, 0);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int c = c0 + u * kProdThreads;
-          if (c >= nchunk) break;
-          if constexpr (R == 1) {
-            *reinterpret_cast<uint4*>(buf + 8 * c) = d[u][0];
-          } else {
-            const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&d[u][0]);
-            const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&d[u][1]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t p = 8 * c + 2 * k;
-              if constexpr (R == 2) {
-                buf[swz<R>(p)] = __byte_perm(w0[k], w1[k], 0x5410);
-                buf[swz<R>(p + 1)] = __byte_perm(w0[k], w1[k], 0x7632);
-              } else {
-                const uint32_t* w2 = reinterpret_cast<const uint32_t*>(&d[u][2]);
-                const uint32_t* w3 = reinterpret_cast<const uint32_t*>(&d[u][3]);
-                buf[swz<R>(p)] = make_uint2(__byte_perm(w0[k], w1[k], 0x5410),
-                                            __byte_perm(w2[k], w3[k], 0x5410));
-                buf[swz<R>(p + 1)] = make_uint2(__byte_perm(w0[k], w1[k], 0x7632),
-                                                __byte_perm(w2[k], w3[k], 0x7632));
-              }
-            }
-          }
+          for (int k = 0; k < 4; ++k)
+            o[k] = make_uint4(__byte_perm(u0[k], u1[k], 0x5410), __byte_perm(u2[k], u3[k], 0x5410),
+                              __byte_perm(u0[k], u1[k], 0x7632), __byte_perm(u2[k], u3[k], 0x7632));
         }
       }
-      named_bar_arrive(1 + slot, kThreads);                  // FULL[slot]
+      ptx::named_bar_sync(1 + grp, gthreads);
     }
-  } else {
-    // ---------------- consumers: gather + quantize + pack + store ------------
-    const int ct = threadIdx.x - kProdThreads;
-    const SegGeom& G = a.geom;
-    const int nvb0 = G.kp[0] / 32, nvb1 = G.kp[1] / 32, nvb2 = G.kp[2] / 32;
-    const int nvb = nvb0 + nvb1 + nvb2;
-    for (int64_t i = 0; i < my_tiles; ++i) {
-      const int slot = int(i & 1);
-      named_bar_sync(1 + slot, kThreads);                    // FULL[slot]
-      const ST* buf = slot ? buf1 : buf0;
-      const int64_t r0 = (blockIdx.x + i * gridDim.x) * R;
-      for (int vb = ct; vb < nvb; vb += kConsThreads) {
-        int g, kb;
-        if (vb < nvb0) { g = 0; kb = vb; }
-        else if (vb < nvb0 + nvb1) { g = 1; kb = vb - nvb0; }
-        else { g = 2; kb = vb - nvb0 - nvb1; }
-        const int kp128 = G.kp[g] / 128;
-        const int bytes_per_blk = g == 0 ? 16 : (g == 1 ? 24 : 32);
-        if (kb * 32 >= G.n[g]) {
-          // padding block: zero codes and zero scale bytes
-#pragma unroll
-          for (int rho = 0; rho < R; ++rho) {
-            const int64_t r = r0 + rho;
-            if (r >= rows_pad) break;
-            a.sf[g][sf_offset(r, kb, kp128)] = 0;
-            if (r < a.rows) {
-              uint8_t* dst = a.codes[g] + r * G.pitch[g] + (int64_t)kb * bytes_per_blk;
-              for (int q = 0; q < bytes_per_blk; q += 8)
-                *reinterpret_cast<uint2*>(dst + q) = make_uint2(0, 0);
-            }
-          }
-          continue;
-        }
-        const int blk = (G.off[g] + 32 * kb) / 32;   // real block index in the reordered row
-        ST vals[32];
-#pragma unroll
-        for (int i2 = 0; i2 < 16; ++i2) {
-          const uint32_t pr = gidx2[i2 * nblk + blk];
-          vals[2 * i2] = buf[pr & 0xFFFFu];
-          vals[2 * i2 + 1] = buf[pr >> 16];
-        }
+    // ---- gather + quantize + pack + store ----
+    if (dbg & 3) { __syncwarp(); if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s])); continue; }
+    const ST* slots = reinterpret_cast<const ST*>(st);
+    const int64_t r0 = (blockIdx.x + i * gridDim.x) * (int64_t)R;
+    const int64_t left = rows - r0;
+    const int nvalid = left >= R ? R : (left > 0 ? (int)left : 0);
+    for (int ch = gw; ch < nch; ch += group_warps) {
+      const int g = ch < nch0 ? 0 : (ch < nch0 + nch1 ? 1 : 2);
+      const int kb = (ch - (g == 0 ? 0 : (g == 1 ? nch0 : nch0 + nch1))) * 32 + lane;
+      const int kp_g = g == 0 ? kp0 : (g == 1 ? kp1 : kp2);
+      if (kb >= kp_g / 32) continue;
+      const int n_g = g == 0 ? n0 : (g == 1 ? n1 : n2);
+      const int off_g = g == 0 ? of0 : (g == 1 ? of1 : of2);
+      const int fmt = g == 1 ? fm1 : fm2;
+      const int off = g == 0 ? so0 : (g == 1 ? so1 : so2);
+      const int64_t pitch = g == 0 ? pt0 : (g == 1 ? pt1 : pt2);
+      uint8_t* sf_g = g == 0 ? sf0 : (g == 1 ? sf1 : sf2);
+      uint8_t* codes_g = g == 0 ? cd0 : (g == 1 ? cd1 : cd2);
+      uint8_t* sfp = sf_g + sf_offset(r0, kb, kp_g / 128);
+      const int bpb = g == 0 ? 16 : (g == 1 ? 24 : 32);
+      uint8_t* crow0 = codes_g + r0 * pitch + (int64_t)kb * bpb;
+      if (kb * 32 >= n_g) {
+        // padding block: zero codes and zero scale bytes
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) {
-          const int64_t r = r0 + rho;
-          if (r >= rows_pad) break;
-          uint32_t v[32];
+          sfp[16 * rho] = 0;
+          if (rho < nvalid)
+            for (int b = 0; b < bpb; b += 8) *reinterpret_cast<uint2*>(crow0 + rho * pitch + b) = make_uint2(0, 0);
+        }
+        continue;
+      }
+      ST v[32];
+      if (use_tab) {
+        const uint32_t* gp = gidx + off_g / 32 + kb;
 #pragma unroll
-          for (int k = 0; k < 32; ++k) v[k] = row_bits<R>(vals[k], rho);
-          uint8_t* crow = a.codes[g] + r * G.pitch[g];
-          quantize_store_block(v, g, G.fmt[g], G.sc_off[g], crow, kb, r < a.rows, a.sf[g], r,
-                               kp128);
+        for (int q = 0; q < 16; ++q) {
+          const uint32_t pr = gp[q * nblk];
+          v[2 * q + 0] = slots[pr & 0xFFFFu];
+          v[2 * q + 1] = slots[pr >> 16];
+        }
+      } else {
+        const int4* pp = reinterpret_cast<const int4*>(a.perm + off_g + 32 * kb);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int4 pv = __ldg(pp + q);
+          v[4 * q + 0] = slots[pv.x];
+          v[4 * q + 1] = slots[pv.y];
+          v[4 * q + 2] = slots[pv.z];
+          v[4 * q + 3] = slots[pv.w];
         }
       }
-      if (i + 2 < my_tiles) named_bar_arrive(1 + 2 + slot, kThreads);  // EMPTY[slot]
+      if (g == 0) quantize_tile_block<R, 0, F_E2M1>(v, off, crow0, pitch, sfp, nvalid);
+      else if (g == 1) {
+        if (fmt == F_E3M2) quantize_tile_block<R, 1, F_E3M2>(v, off, crow0, pitch, sfp, nvalid);
+        else quantize_tile_block<R, 1, F_E2M3>(v, off, crow0, pitch, sfp, nvalid);
+      } else {
+        if (fmt == F_E4M3) quantize_tile_block<R, 2, F_E4M3>(v, off, crow0, pitch, sfp, nvalid);
+        else quantize_tile_block<R, 2, F_E5M2>(v, off, crow0, pitch, sfp, nvalid);
+      }
     }
+    // ---- release the stage (every warp of the group arrives once) ----
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s]));
   }
 }
 
@@ -293,20 +450,64 @@ __global__ void reorder_bf16_kernel(const uint16_t* __restrict__ x, int64_t rows
 
 template <int R>
 cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
-  const size_t gbytes = ((size_t)a.K * 2 + 127) / 128 * 128;
-  const size_t smem = gbytes + 2 * (size_t)a.K * sizeof(typename SlotT<R>::T);
-  cudaError_t e = cudaFuncSetAttribute(rq_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
+  EncodeTiledFn enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  RqDev d{};
+  d.a = a;
   const int64_t rows_pad = (a.rows + 127) / 128 * 128;
-  const int64_t n_tiles = (rows_pad + R - 1) / R;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rq_kernel<R>, kThreads, smem);
+  d.n_tiles = rows_pad / R;
+  d.nbox = (a.K + 255) / 256;
+  const size_t stage_bytes = (size_t)d.nbox * 512 * R;
+  // Stage the permutation in smem (gather table) when that still leaves >= 3 stages.
+  d.perm_smem = (200 * 1024 - (size_t)a.K * 6) / stage_bytes >= 3 ? 1 : 0;
+  const size_t tab_bytes = d.perm_smem ? (size_t)a.K * 6 : 0;
+  int stages = (int)((200 * 1024 - tab_bytes) / stage_bytes);
+  if (stages > 8) stages = 8;
+  { const char* e = getenv("MM_RQ_STAGES"); if (e && atoi(e) >= 2 && atoi(e) < stages) stages = atoi(e); }
+  if (stages < 2) return cudaErrorInvalidConfiguration;
+  d.stages = stages;
+  int gw = (a.geom.kp[0] / 32 + 31) / 32 + (a.geom.kp[1] / 32 + 31) / 32 + (a.geom.kp[2] / 32 + 31) / 32;
+  if (gw > 8) gw = 8;
+  if (gw < 2) gw = 2;
+  d.group_warps = gw;
+  int groups = 15 / gw;   // <= 15 consumer warps + the producer warp
+  if (groups > stages - 1) groups = stages - 1;
+  if (groups < 1) groups = 1;
+  d.groups = groups;
+  { const char* e = getenv("MM_RQ_DEBUG"); d.dbg = e ? atoi(e) : 0; }
+  // TMA map over X.  Preferred: a 3-D view {256 channels, rows, K/256 boxes} with
+  // strides {ldx*2, 512 B}, so ONE load per tile lands box-major ([box][R][256]);
+  // else (K % 256 != 0, or the driver rejects the view) 2-D boxes of 256 x R.
+  CUtensorMap m;
+  d.box3d = 0;
+  const char* no3d = getenv("MM_RQ_NO3D");   // timing experiments only
+  if (a.K % 256 == 0 && d.nbox <= 256 && !(no3d && atoi(no3d))) {
+    cuuint64_t dims[3] = {256, (cuuint64_t)a.rows, (cuuint64_t)d.nbox};
+    cuuint64_t strides[2] = {(cuuint64_t)a.ldx * 2, 512};
+    cuuint32_t box[3] = {256, (cuuint32_t)R, (cuuint32_t)d.nbox};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t*>(a.x), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      d.box3d = 1;
+  }
+  if (!d.box3d) {
+    cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.rows};
+    cuuint64_t strides[1] = {(cuuint64_t)a.ldx * 2};
+    cuuint32_t box[2] = {256, (cuuint32_t)R};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t*>(a.x), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + tab_bytes + (2 * stages + 1) * 8;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(rq_kernel<R>), smem);
   if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  int64_t grid = (int64_t)sm_count() * per_sm;
-  if (grid > n_tiles) grid = n_tiles;
-  rq_kernel<R><<<(unsigned)grid, kThreads, smem, s>>>(a, rows_pad, n_tiles);
+  const int threads = 32 * (1 + groups * gw);
+  int64_t grid = sm_count();
+  if (grid > d.n_tiles) grid = d.n_tiles;
+  rq_kernel<R><<<(unsigned)grid, threads, smem, s>>>(m, d);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
@@ -314,11 +515,11 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
 }  // namespace
 
 cudaError_t launch_reorder_quantize(const RqArgs& a, cudaStream_t s, int64_t* launches) {
-  // Rows per tile: as many as keep two tiles of smem within ~100 KB (R = 4 for
-  // Llama/Qwen hidden sizes, R = 2 / 1 for the wide down_proj inputs).
-  const size_t row_bytes = (size_t)a.K * 2;
-  if (4 * row_bytes * 2 <= 100 * 1024) return launch_rq_t<4>(a, s, launches);
-  if (2 * row_bytes * 2 <= 150 * 1024) return launch_rq_t<2>(a, s, launches);
+  if (a.rows == 0) return cudaSuccess;
+  // Rows per tile: 4 while a stage of 4 rows leaves room for >= 4 stages, then 2, 1.
+  const size_t row_bytes = (size_t)((a.K + 255) / 256) * 512;
+  if (4 * row_bytes * 4 <= 200 * 1024) return launch_rq_t<4>(a, s, launches);
+  if (2 * row_bytes * 3 <= 200 * 1024) return launch_rq_t<2>(a, s, launches);
   return launch_rq_t<1>(a, s, launches);
 }
 
