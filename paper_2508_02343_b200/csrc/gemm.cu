@@ -278,43 +278,6 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
   if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
 }
 
-// ---------------------------------------------------------------------------- host
-// 2-D K-major operand map: inner dim = K coordinate (bytes, or FP6 elements),
-// outer = rows; box = 128 x box_rows; 128-byte swizzle.
-bool make_operand_map(CUtensorMap* m, const void* base, int g, int kp, int64_t rows, int64_t pitch,
-                      int box_rows) {
-  EncodeTiledFn enc = tensor_map_encoder();
-  if (!enc) return false;
-  CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_UINT8;
-  cuuint64_t inner;
-  if (g == 0) inner = kp / 2;
-  else if (g == 1) { dt = CU_TENSOR_MAP_DATA_TYPE_16U6_ALIGN16B; inner = kp; }
-  else inner = kp;
-  cuuint64_t dims[2] = {inner, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)pitch};
-  cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-uint32_t make_idesc(int fmt, int g, int n) {
-  uint32_t code;
-  if (g == 0) code = 1;  // kind::mxf4 E2M1
-  else {
-    switch (fmt) {
-      case F_E4M3: code = 0; break;
-      case F_E5M2: code = 1; break;
-      case F_E2M3: code = 3; break;
-      case F_E3M2: code = 4; break;
-      default: code = 5; break;
-    }
-  }
-  return (code << 7) | (code << 10) | ((uint32_t)(n >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
-}
-
 template <int BN, int STAGES>
 size_t smem_bytes() {
   using C = Cfg<BN, STAGES>;
@@ -354,7 +317,7 @@ cudaError_t run(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_
     p.nst[g] = g == 0 ? (a.geom.kp[0] + 255) / 256 : a.geom.kp[g] / 128;
     p.sfa[g] = a.a_sf[g];
     p.sfb[g] = a.w_sf[g];
-    p.idesc[g] = make_idesc(a.geom.fmt[g], g, BN);
+    p.idesc[g] = make_idesc_mn(a.geom.fmt[g], g, BM, BN);
   }
   p.sfb_rows_pad = (a.N + 127) / 128 * 128;
   p.y = a.y;
@@ -375,6 +338,43 @@ cudaError_t run(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_
 
 }  // namespace
 
+// 2-D K-major operand map: inner dim = K coordinate (bytes, or FP6 elements),
+// outer = rows; box = 128 x box_rows; 128-byte swizzle.
+bool make_operand_map(CUtensorMap* m, const void* base, int g, int kp, int64_t rows, int64_t pitch,
+                      int box_rows) {
+  EncodeTiledFn enc = tensor_map_encoder();
+  if (!enc) return false;
+  CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  cuuint64_t inner;
+  if (g == 0) inner = kp / 2;
+  else if (g == 1) { dt = CU_TENSOR_MAP_DATA_TYPE_16U6_ALIGN16B; inner = kp; }
+  else inner = kp;
+  cuuint64_t dims[2] = {inner, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch};
+  cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+uint32_t make_idesc_mn(int fmt, int g, int m, int n) {
+  uint32_t code;
+  if (g == 0) code = 1;  // kind::mxf4 E2M1
+  else {
+    switch (fmt) {
+      case F_E4M3: code = 0; break;
+      case F_E5M2: code = 1; break;
+      case F_E2M3: code = 3; break;
+      case F_E3M2: code = 4; break;
+      default: code = 5; break;
+    }
+  }
+  return (code << 7) | (code << 10) | ((uint32_t)(n >> 3) << 17) | (1u << 23) | ((uint32_t)(m >> 4) << 24);
+}
+
+
 EncodeTiledFn tensor_map_encoder() {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
@@ -391,7 +391,9 @@ EncodeTiledFn tensor_map_encoder() {
 cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
                               const char** err) {
   int bn = cfg.block_n;
-  if (bn == 0) bn = 256;
+  // auto: CTA-pair 256 x 256 tiles once M fills a pair tile's rows, else single-CTA 128 x 256
+  if (bn == 0) bn = a.M > 128 ? 512 : 256;
+  if (bn == 512) return launch_mixed_gemm_2cta(a, cfg, s, launches, err);
   if (bn == 128) {
     if (cfg.num_stages == 4) return run<128, 4>(a, cfg, s, launches, err);
     return run<128, 6>(a, cfg, s, launches, err);

@@ -1,0 +1,335 @@
+// gemm2.cu -- the MicroMix mixed block-scaled GEMM on CTA PAIRS (tcgen05
+// cta_group::2), sm_100a.  PAPER.md §3.2 "GEMM Kernel" (line 143), Fig. 5 (line
+// 137), Eq. 2 (lines 47-51): Y[M, N] (BF16) = sum over the MXFP4 / MXFP6 / MXFP8
+// K-segments of A_g W_g^T with E8M0 block scales, one FP32 accumulator.
+//
+// Same stage structure as gemm.cu (every stage = 128-byte smem rows: an FP4
+// stage covers 256 K with 4 x kind::mxf4 K=64, an FP6 or FP8 stage 128 K with
+// 4 x kind::mxf8f6f4 K=32; one persistent K loop over the three segments into one
+// TMEM accumulator), but the output tile is 256 x 256 per CTA PAIR: each CTA of
+// the pair loads its 128 rows of A and its 128 rows of W (half of N) per stage,
+// the even CTA issues tcgen05.mma.cta_group::2 (M = 256, N = 256) which reads both
+// CTAs' shared memory, and each CTA's TMEM holds its 128 rows x 256 columns.  Per
+// CTA and stage that is 32 KB of operand traffic for a 128 x 256 x K_stage slab
+// (the single-CTA 128 x 256 tile needs 48 KB): the L2 -> SM traffic, which bounds
+// the single-CTA kernel, drops by a third.
+//
+// Roles (per CTA, 256 threads): warp 0 = TMA producer (operand tiles and scale
+// atoms; completions land on the even CTA's full barrier), warp 1 = MMA issuer
+// (even CTA only: tcgen05.cp of the scale atoms + the MMAs, commits multicast to
+// both CTAs), warp 2 = TMEM allocator, warps 4-7 = epilogue (tcgen05.ld -> BF16).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdlib>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace mmx {
+namespace {
+
+constexpr int kThreads2 = 256;
+constexpr int A_BYTES = 128 * 128;       // this CTA's 128 rows x 128 B
+constexpr int B_BYTES = 128 * 128;       // this CTA's 128 W rows x 128 B
+constexpr int SFA_BYTES = 2 * 512;       // up to 2 atoms (FP4 stage)
+constexpr int SFB_BYTES = 2 * 2 * 512;   // 2 row groups (N = 256) x up to 2 atoms
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
+constexpr int SF_STRIDE = 24;            // TMEM columns per stage: SFA 2x4, SFB 2x2x4
+
+struct Gemm2Dev {
+  int64_t M, N;
+  int num_m2, num_n, num_tiles;   // pair tiles of 256 x 256
+  int nst0, nst1, nst2;           // stages per segment
+  int n0, n1, n2;                 // real channels per segment
+  int kp0, kp1, kp2;              // stored channels per segment
+  uint32_t idesc0, idesc1, idesc2;
+  uint16_t* y;
+  int64_t ldy;
+};
+
+template <int G>
+__device__ __forceinline__ void seg_stage(const Gemm2Dev& p, int j, int& kcoord, int& nmma, int& atoms, int& atom0) {
+  const int n = G == 0 ? p.n0 : (G == 1 ? p.n1 : p.n2);
+  const int kp = G == 0 ? p.kp0 : (G == 1 ? p.kp1 : p.kp2);
+  if constexpr (G == 0) {
+    kcoord = 128 * j;                               // bytes (2 E2M1 per byte)
+    nmma = (min(n - 256 * j, 256) + 63) / 64;
+    atoms = min(kp - 256 * j, 256) / 128;
+    atom0 = 2 * j;
+  } else {
+    kcoord = 128 * j;                               // FP6: elements, FP8: bytes
+    nmma = (min(n - 128 * j, 128) + 31) / 32;
+    atoms = 1;
+    atom0 = j;
+  }
+}
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
+mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
+                const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb0,
+                const __grid_constant__ CUtensorMap tb1, const __grid_constant__ CUtensorMap tb2,
+                const __grid_constant__ CUtensorMap tsa0, const __grid_constant__ CUtensorMap tsa1,
+                const __grid_constant__ CUtensorMap tsa2, const __grid_constant__ CUtensorMap tsb0,
+                const __grid_constant__ CUtensorMap tsb1, const __grid_constant__ CUtensorMap tsb2,
+                const __grid_constant__ Gemm2Dev p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * A_BYTES;
+  uint8_t* sSFA = sB + STAGES * B_BYTES;
+  uint8_t* sSFB = sSFA + STAGES * SFA_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSFB + STAGES * SFB_BYTES);
+  uint64_t* full = bars;                  // [STAGES]  (used in the even CTA)
+  uint64_t* empty = bars + STAGES;        // [STAGES]  (each CTA)
+  uint64_t* tfull = bars + 2 * STAGES;    // [1]       (each CTA)
+  uint64_t* tempty = tfull + 1;           // [1]       (even CTA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_ctarank();    // 0 = MMA leader
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&ta0); ptx::tma_prefetch_desc(&ta1); ptx::tma_prefetch_desc(&ta2);
+    ptx::tma_prefetch_desc(&tb0); ptx::tma_prefetch_desc(&tb1); ptx::tma_prefetch_desc(&tb2);
+    ptx::tma_prefetch_desc(&tsa0); ptx::tma_prefetch_desc(&tsa1); ptx::tma_prefetch_desc(&tsa2);
+    ptx::tma_prefetch_desc(&tsb0); ptx::tma_prefetch_desc(&tsb1); ptx::tma_prefetch_desc(&tsb2);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), 1);
+    }
+    ptx::mbar_init(ptx::smem_u32(tfull), 1);
+    ptx::mbar_init(ptx::smem_u32(tempty), 8);     // 4 epilogue warps x 2 CTAs
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), 512);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t M = p.M, N = p.N;
+  const int num_m2 = p.num_m2, num_tiles = p.num_tiles;
+
+  if (warp == 0) {
+    // ============================ TMA producer (both CTAs) ============================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t full0 = ptx::smem_u32(&full[0]);
+      for (int t = pair; t < num_tiles; t += npairs) {
+        const int mb2 = t % num_m2, nb = t / num_m2;
+        const int m0 = mb2 * 256 + 128 * (int)rank;      // this CTA's A rows
+        const int n0 = nb * 256 + 128 * (int)rank;       // this CTA's W rows (its half of N)
+        const int mgrp = mb2 * 2 + (int)rank;           // 128-row scale group of A
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+          const int nst = g == 0 ? p.nst0 : (g == 1 ? p.nst1 : p.nst2);
+          const int kp128 = (g == 0 ? p.kp0 : (g == 1 ? p.kp1 : p.kp2)) / 128;
+          const CUtensorMap* ta = g == 0 ? &ta0 : (g == 1 ? &ta1 : &ta2);
+          const CUtensorMap* tb = g == 0 ? &tb0 : (g == 1 ? &tb1 : &tb2);
+          const CUtensorMap* tsa = g == 0 ? &tsa0 : (g == 1 ? &tsa1 : &tsa2);
+          const CUtensorMap* tsb = g == 0 ? &tsb0 : (g == 1 ? &tsb1 : &tsb2);
+          const int box_atoms = g == 0 ? 2 : 1;
+          // TMA counts GLOBAL element bits: a 16U6 (FP6) box of 128 elements lands
+          // as 128 B per smem row but completes 96 B per row.
+          const uint32_t ab = g == 1 ? (A_BYTES + B_BYTES) / 4 * 3 : (A_BYTES + B_BYTES);
+          const uint32_t cta_bytes = ab + 3u * box_atoms * 512u;
+          for (int j = 0; j < nst; ++j) {
+            int kcoord, nmma, atoms, atom0;
+            if (g == 0) seg_stage<0>(p, j, kcoord, nmma, atoms, atom0);
+            else if (g == 1) seg_stage<1>(p, j, kcoord, nmma, atoms, atom0);
+            else seg_stage<2>(p, j, kcoord, nmma, atoms, atom0);
+            ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1, 21, stage, t);
+            const uint32_t fb = full0 + 8 * stage;     // the even CTA's barrier (peer bit cleared)
+            if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * cta_bytes);
+            ptx::tma_load_2d_cg2(ptx::smem_u32(sA + stage * A_BYTES), ta, fb, kcoord, m0);
+            ptx::tma_load_2d_cg2(ptx::smem_u32(sB + stage * B_BYTES), tb, fb, kcoord, n0);
+            ptx::tma_load_2d_cg2(ptx::smem_u32(sSFA + stage * SFA_BYTES), tsa, fb, 0, mgrp * kp128 + atom0);
+#pragma unroll
+            for (int rg = 0; rg < 2; ++rg)
+              ptx::tma_load_2d_cg2(ptx::smem_u32(sSFB + stage * SFB_BYTES + rg * 1024), tsb, fb, 0,
+                                   (nb * 2 + rg) * kp128 + atom0);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer (even CTA) ============================
+    if (rank == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < num_tiles; t += npairs, ++it) {
+        ptx::mbar_wait(ptx::smem_u32(tempty), (it & 1) ^ 1, 22, it, t);
+        ptx::tc_fence_after();
+        bool first = true;
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+          const int nst = g == 0 ? p.nst0 : (g == 1 ? p.nst1 : p.nst2);
+          const uint32_t idesc = g == 0 ? p.idesc0 : (g == 1 ? p.idesc1 : p.idesc2);
+          for (int j = 0; j < nst; ++j) {
+            int kcoord, nmma, atoms, atom0;
+            if (g == 0) seg_stage<0>(p, j, kcoord, nmma, atoms, atom0);
+            else if (g == 1) seg_stage<1>(p, j, kcoord, nmma, atoms, atom0);
+            else seg_stage<2>(p, j, kcoord, nmma, atoms, atom0);
+            ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase, 23, stage, t);
+            ptx::tc_fence_after();
+            if (lane == 0) {
+              const uint32_t sfa_t = tmem_base + 256 + stage * SF_STRIDE;
+              const uint32_t sfb_t = sfa_t + 8;
+              for (int at = 0; at < atoms; ++at) {
+                ptx::tc_cp_32x128b_x4_cg2(sfa_t + 4 * at,
+                                          ptx::smem_desc(ptx::smem_u32(sSFA + stage * SFA_BYTES + at * 512), 0, 128, 0));
+#pragma unroll
+                for (int rg = 0; rg < 2; ++rg)
+                  ptx::tc_cp_32x128b_x4_cg2(
+                      sfb_t + (at * 2 + rg) * 4,
+                      ptx::smem_desc(ptx::smem_u32(sSFB + stage * SFB_BYTES + rg * 1024 + at * 512), 0, 128, 0));
+              }
+              const uint32_t a_base = ptx::smem_u32(sA + stage * A_BYTES);
+              const uint32_t b_base = ptx::smem_u32(sB + stage * B_BYTES);
+              for (int k = 0; k < nmma; ++k) {
+                const uint64_t ad = ptx::smem_desc(a_base + 32 * k, 16, 1024, 2);
+                const uint64_t bd = ptx::smem_desc(b_base + 32 * k, 16, 1024, 2);
+                const uint32_t accum = first ? 0u : 1u;
+                first = false;
+                if (g == 0) {
+                  const uint32_t sid = 2u * (k & 1);
+                  ptx::tc_mma_mxf4_cg2(tmem_base, ad, bd, idesc | (sid << 29) | (sid << 4), sfa_t + 4 * (k >> 1),
+                                       sfb_t + (k >> 1) * 8, accum);
+                } else {
+                  ptx::tc_mma_mxf8f6f4_cg2(tmem_base, ad, bd, idesc | ((uint32_t)k << 29) | ((uint32_t)k << 4), sfa_t,
+                                           sfb_t, accum);
+                }
+              }
+              ptx::tc_commit_cg2_mc(ptx::smem_u32(&empty[stage]), 0x3);
+            }
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+        if (lane == 0) ptx::tc_commit_cg2_mc(ptx::smem_u32(tfull), 0x3);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ============================ epilogue (both CTAs) ============================
+    const int q = warp & 3;                           // TMEM lane quadrant
+    const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);
+    int it = 0;
+    for (int t = pair; t < num_tiles; t += npairs, ++it) {
+      const int mb2 = t % num_m2, nb = t / num_m2;
+      ptx::mbar_wait(ptx::smem_u32(tfull), it & 1, 24, it, t);
+      ptx::tc_fence_after();
+      const int64_t row = (int64_t)mb2 * 256 + 128 * rank + q * 32 + lane;
+      const int64_t n0 = (int64_t)nb * 256;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + 32 * c, r);
+        ptx::tc_wait_ld();
+        if (row < M) {
+          uint16_t* yrow = p.y + row * p.ldy + n0 + 32 * c;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            if (n0 + 32 * c + 8 * v < N) {
+              uint4 o;
+              o.x = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
+              o.y = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
+              o.z = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
+              o.w = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+              *reinterpret_cast<uint4*>(yrow + 8 * v) = o;
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc_cg2(tmem_base, 512);
+}
+
+// Scale-factor map: the atoms of one operand segment viewed as a 2-D array of
+// [n_atoms][128 x u32] (512-byte atoms, see include/mm.h), box = box_atoms atoms.
+bool make_sf_map(CUtensorMap* m, const void* base, int64_t rows, int kp, int box_atoms) {
+  EncodeTiledFn enc = tensor_map_encoder();
+  if (!enc) return false;
+  const int64_t n_atoms = (rows + 127) / 128 * (kp / 128);
+  cuuint64_t dims[2] = {128, (cuuint64_t)n_atoms};
+  cuuint64_t strides[1] = {512};
+  cuuint32_t box[2] = {128, (cuuint32_t)box_atoms};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int STAGES>
+cudaError_t run2(const GemmArgs& a, cudaStream_t s, int64_t* launches, const char** err) {
+  CUtensorMap maps[12];
+  int first = -1;
+  for (int g = 0; g < 3; ++g) {
+    if (a.geom.n[g] == 0) continue;
+    const int box_atoms = g == 0 ? 2 : 1;
+    if (!make_operand_map(&maps[g], a.a_codes[g], g, a.geom.kp[g], a.M, a.geom.pitch[g], 128) ||
+        !make_operand_map(&maps[3 + g], a.w_codes[g], g, a.geom.kp[g], a.N, a.geom.pitch[g], 128) ||
+        !make_sf_map(&maps[6 + g], a.a_sf[g], a.M, a.geom.kp[g], box_atoms) ||
+        !make_sf_map(&maps[9 + g], a.w_sf[g], a.N, a.geom.kp[g], box_atoms)) {
+      *err = "cuTensorMapEncodeTiled failed";
+      return cudaErrorInvalidValue;
+    }
+    if (first < 0) first = g;
+  }
+  if (first < 0) { *err = "empty plan"; return cudaErrorInvalidValue; }
+  for (int g = 0; g < 3; ++g)
+    if (a.geom.n[g] == 0)
+      for (int k = 0; k < 4; ++k) maps[3 * k + g] = maps[3 * k + first];   // valid, never used
+  Gemm2Dev p{};
+  p.M = a.M;
+  p.N = a.N;
+  p.num_m2 = (int)((a.M + 255) / 256);
+  p.num_n = (int)((a.N + 255) / 256);
+  p.num_tiles = p.num_m2 * p.num_n;
+  p.nst0 = (a.geom.kp[0] + 255) / 256;
+  p.nst1 = a.geom.kp[1] / 128;
+  p.nst2 = a.geom.kp[2] / 128;
+  p.n0 = a.geom.n[0]; p.n1 = a.geom.n[1]; p.n2 = a.geom.n[2];
+  p.kp0 = a.geom.kp[0]; p.kp1 = a.geom.kp[1]; p.kp2 = a.geom.kp[2];
+  p.idesc0 = make_idesc_mn(a.geom.fmt[0], 0, 256, 256);
+  p.idesc1 = make_idesc_mn(a.geom.fmt[1], 1, 256, 256);
+  p.idesc2 = make_idesc_mn(a.geom.fmt[2], 2, 256, 256);
+  p.y = a.y;
+  p.ldy = a.ldy;
+  if (p.num_tiles == 0) return cudaSuccess;
+  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + (2 * STAGES + 2) * 8 + 16;
+  auto kern = mixgemm2_kernel<STAGES>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
+  int grid = sm_count() & ~1;
+  if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
+  kern<<<grid, kThreads2, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7],
+                                     maps[8], maps[9], maps[10], maps[11], p);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_mixed_gemm_2cta(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
+                                   const char** err) {
+  if (cfg.num_stages == 5) return run2<5>(a, s, launches, err);
+  return run2<6>(a, s, launches, err);
+}
+
+}  // namespace mmx

@@ -78,6 +78,14 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 EncodeTiledFn tensor_map_encoder();
 
+// 2-D K-major operand map of segment g (inner = K bytes, or FP6 elements via the
+// 16U6_ALIGN16B type; box 128 x box_rows; 128-byte swizzle) and the block-scaled
+// tcgen05 instruction descriptor for an M x N MMA of segment g (gemm.cu).
+bool make_operand_map(CUtensorMap* m, const void* base, int g, int kp, int64_t rows, int64_t pitch, int box_rows);
+uint32_t make_idesc_mn(int fmt, int g, int m, int n);
+cudaError_t launch_mixed_gemm_2cta(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
+                                   const char** err);
+
 // Host-side launch caches (per device, thread-safe): raise a kernel's dynamic
 // shared-memory limit once, and remember occupancy queries, so the hot calls do
 // no redundant driver work per launch.
