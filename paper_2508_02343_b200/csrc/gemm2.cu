@@ -36,6 +36,7 @@ constexpr int SFA_BYTES = 2 * 512;       // up to 2 atoms (FP4 stage)
 constexpr int SFB_BYTES = 2 * 2 * 512;   // 2 row groups (N = 256) x up to 2 atoms
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
 constexpr int SF_STRIDE = 24;            // TMEM columns per stage: SFA 2x4, SFB 2x2x4
+constexpr int EPI_BYTES = 4 * 2 * 32 * 64;  // epilogue staging: 4 warps x 2 buffers x (32 x 32 BF16)
 
 struct Gemm2Dev {
   int64_t M, N;
@@ -46,6 +47,7 @@ struct Gemm2Dev {
   uint32_t idesc0, idesc1, idesc2;
   uint16_t* y;
   int64_t ldy;
+  int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
 };
 
 template <int G>
@@ -73,14 +75,15 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
                 const __grid_constant__ CUtensorMap tsa0, const __grid_constant__ CUtensorMap tsa1,
                 const __grid_constant__ CUtensorMap tsa2, const __grid_constant__ CUtensorMap tsb0,
                 const __grid_constant__ CUtensorMap tsb1, const __grid_constant__ CUtensorMap tsb2,
-                const __grid_constant__ Gemm2Dev p) {
+                const __grid_constant__ CUtensorMap ty, const __grid_constant__ Gemm2Dev p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * A_BYTES;
   uint8_t* sSFA = sB + STAGES * B_BYTES;
   uint8_t* sSFB = sSFA + STAGES * SFA_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sSFB + STAGES * SFB_BYTES);
+  uint8_t* sEpi = sSFB + STAGES * SFB_BYTES;      // [4 warps][2][32 rows x 64 B] BF16 staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_BYTES);
   uint64_t* full = bars;                  // [STAGES]  (used in the even CTA)
   uint64_t* empty = bars + STAGES;        // [STAGES]  (each CTA)
   uint64_t* tfull = bars + 2 * STAGES;    // [1]       (each CTA)
@@ -145,14 +148,22 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
             else seg_stage<2>(p, j, kcoord, nmma, atoms, atom0);
             ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1, 21, stage, t);
             const uint32_t fb = full0 + 8 * stage;     // the even CTA's barrier (peer bit cleared)
-            if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * cta_bytes);
+            const bool no_sf = (p.dbg & 8) != 0;   // timing experiment only
+            if (p.dbg & 16) {                      // timing experiment: no loads at all
+              if (rank == 0) ptx::mbar_arrive(fb);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+              continue;
+            }
+            if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * (no_sf ? ab : cta_bytes));
             ptx::tma_load_2d_cg2(ptx::smem_u32(sA + stage * A_BYTES), ta, fb, kcoord, m0);
             ptx::tma_load_2d_cg2(ptx::smem_u32(sB + stage * B_BYTES), tb, fb, kcoord, n0);
-            ptx::tma_load_2d_cg2(ptx::smem_u32(sSFA + stage * SFA_BYTES), tsa, fb, 0, mgrp * kp128 + atom0);
+            if (!no_sf) {
+              ptx::tma_load_2d_cg2(ptx::smem_u32(sSFA + stage * SFA_BYTES), tsa, fb, 0, mgrp * kp128 + atom0);
 #pragma unroll
-            for (int rg = 0; rg < 2; ++rg)
-              ptx::tma_load_2d_cg2(ptx::smem_u32(sSFB + stage * SFB_BYTES + rg * 1024), tsb, fb, 0,
-                                   (nb * 2 + rg) * kp128 + atom0);
+              for (int rg = 0; rg < 2; ++rg)
+                ptx::tma_load_2d_cg2(ptx::smem_u32(sSFB + stage * SFB_BYTES + rg * 1024), tsb, fb, 0,
+                                     (nb * 2 + rg) * kp128 + atom0);
+            }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }
@@ -160,98 +171,126 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     }
   } else if (warp == 1) {
     // ============================ MMA issuer (even CTA) ============================
+    // The whole warp runs this loop converged; elect.sync inside the issue blocks
+    // picks the one lane that issues (operands stay warp-uniform).  Full stages go
+    // through one asm block each (scale copies + 4 MMAs + commit); only a segment's
+    // last stage may issue fewer MMAs and takes the per-MMA path.
     if (rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      const uint32_t sA0 = ptx::smem_u32(sA), sB0 = ptx::smem_u32(sB);
+      const uint32_t sSFA0 = ptx::smem_u32(sSFA), sSFB0 = ptx::smem_u32(sSFB);
+      const uint32_t empty0 = ptx::smem_u32(&empty[0]), full0 = ptx::smem_u32(&full[0]);
+      const bool no_mma = (p.dbg & 2) != 0;
       for (int t = pair; t < num_tiles; t += npairs, ++it) {
         ptx::mbar_wait(ptx::smem_u32(tempty), (it & 1) ^ 1, 22, it, t);
         ptx::tc_fence_after();
-        bool first = true;
+        uint32_t accum = 0;
 #pragma unroll
         for (int g = 0; g < 3; ++g) {
           const int nst = g == 0 ? p.nst0 : (g == 1 ? p.nst1 : p.nst2);
+          const int n_g = g == 0 ? p.n0 : (g == 1 ? p.n1 : p.n2);
           const uint32_t idesc = g == 0 ? p.idesc0 : (g == 1 ? p.idesc1 : p.idesc2);
+          const int kstage = g == 0 ? 256 : 128;                    // K per stage
+          const int kmma = g == 0 ? 64 : 32;                        // K per MMA
           for (int j = 0; j < nst; ++j) {
-            int kcoord, nmma, atoms, atom0;
-            if (g == 0) seg_stage<0>(p, j, kcoord, nmma, atoms, atom0);
-            else if (g == 1) seg_stage<1>(p, j, kcoord, nmma, atoms, atom0);
-            else seg_stage<2>(p, j, kcoord, nmma, atoms, atom0);
-            ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase, 23, stage, t);
+            const int nmma = min((n_g - kstage * j + kmma - 1) / kmma, 4);
+            ptx::mbar_wait(full0 + 8 * stage, phase, 23, stage, t);
             ptx::tc_fence_after();
-            if (lane == 0) {
-              const uint32_t sfa_t = tmem_base + 256 + stage * SF_STRIDE;
-              const uint32_t sfb_t = sfa_t + 8;
-              for (int at = 0; at < atoms; ++at) {
-                ptx::tc_cp_32x128b_x4_cg2(sfa_t + 4 * at,
-                                          ptx::smem_desc(ptx::smem_u32(sSFA + stage * SFA_BYTES + at * 512), 0, 128, 0));
-#pragma unroll
-                for (int rg = 0; rg < 2; ++rg)
-                  ptx::tc_cp_32x128b_x4_cg2(
-                      sfb_t + (at * 2 + rg) * 4,
-                      ptx::smem_desc(ptx::smem_u32(sSFB + stage * SFB_BYTES + rg * 1024 + at * 512), 0, 128, 0));
-              }
-              const uint32_t a_base = ptx::smem_u32(sA + stage * A_BYTES);
-              const uint32_t b_base = ptx::smem_u32(sB + stage * B_BYTES);
-              for (int k = 0; k < nmma; ++k) {
-                const uint64_t ad = ptx::smem_desc(a_base + 32 * k, 16, 1024, 2);
-                const uint64_t bd = ptx::smem_desc(b_base + 32 * k, 16, 1024, 2);
-                const uint32_t accum = first ? 0u : 1u;
-                first = false;
-                if (g == 0) {
-                  const uint32_t sid = 2u * (k & 1);
-                  ptx::tc_mma_mxf4_cg2(tmem_base, ad, bd, idesc | (sid << 29) | (sid << 4), sfa_t + 4 * (k >> 1),
-                                       sfb_t + (k >> 1) * 8, accum);
-                } else {
-                  ptx::tc_mma_mxf8f6f4_cg2(tmem_base, ad, bd, idesc | ((uint32_t)k << 29) | ((uint32_t)k << 4), sfa_t,
-                                           sfb_t, accum);
+            const uint32_t sfa_t = tmem_base + 256 + stage * SF_STRIDE;
+            const uint32_t sfb_t = sfa_t + 8;
+            const uint64_t ad = ptx::smem_desc(sA0 + stage * A_BYTES, 16, 1024, 2);
+            const uint64_t bd = ptx::smem_desc(sB0 + stage * B_BYTES, 16, 1024, 2);
+            const uint64_t sda = ptx::smem_desc(sSFA0 + stage * SFA_BYTES, 0, 128, 0);
+            const uint64_t sdb0 = ptx::smem_desc(sSFB0 + stage * SFB_BYTES, 0, 128, 0);
+            const uint64_t sdb1 = ptx::smem_desc(sSFB0 + stage * SFB_BYTES + 1024, 0, 128, 0);
+            if (nmma == 4 && !no_mma) {
+              if (g == 0) ptx::stage_f4_cg2(tmem_base, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage);
+              else ptx::stage_f8f6_cg2(tmem_base, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage);
+              accum = 1;
+            } else {
+              // partial stage: scale copies for the atoms it uses, then nmma MMAs
+              if (lane == 0) {
+                const int atoms = g == 0 ? (nmma + 1) / 2 : 1;
+                for (int at = 0; at < atoms; ++at) {
+                  ptx::tc_cp_32x128b_x4_cg2(sfa_t + 4 * at, sda + 32 * at);
+                  ptx::tc_cp_32x128b_x4_cg2(sfb_t + 8 * at, sdb0 + 32 * at);
+                  ptx::tc_cp_32x128b_x4_cg2(sfb_t + 8 * at + 4, sdb1 + 32 * at);
                 }
+                for (int k = 0; k < (no_mma ? 0 : nmma); ++k) {
+                  if (g == 0) {
+                    const uint32_t sid = 2u * (k & 1);
+                    ptx::tc_mma_mxf4_cg2(tmem_base, ad + 2 * k, bd + 2 * k, idesc | (sid << 29) | (sid << 4),
+                                         sfa_t + 4 * (k >> 1), sfb_t + (k >> 1) * 8, accum);
+                  } else {
+                    ptx::tc_mma_mxf8f6f4_cg2(tmem_base, ad + 2 * k, bd + 2 * k, idesc | ((uint32_t)k << 29) | ((uint32_t)k << 4),
+                                             sfa_t, sfb_t, accum);
+                  }
+                  accum = 1;
+                }
+                ptx::tc_commit_cg2_mc(empty0 + 8 * stage, 0x3);
               }
-              ptx::tc_commit_cg2_mc(ptx::smem_u32(&empty[stage]), 0x3);
+              accum = __shfl_sync(0xffffffffu, accum, 0);
+              __syncwarp();
             }
-            __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }
-        if (lane == 0) ptx::tc_commit_cg2_mc(ptx::smem_u32(tfull), 0x3);
+        ptx::commit_cg2_mc_elect(ptx::smem_u32(tfull));
         __syncwarp();
       }
     }
   } else if (warp >= 4) {
     // ============================ epilogue (both CTAs) ============================
+    // Per 32-column chunk: tcgen05.ld (32 lanes x 32 columns) -> BF16 RNE -> this
+    // warp's smem staging buffer -> one TMA store of the 32 x 32 box (the TMA clips
+    // rows >= M and columns >= N).  Two staging buffers per warp let the next
+    // chunk's conversion overlap the previous store; the accumulator is released to
+    // the MMA warp as soon as its last chunk is in registers.
     const int q = warp & 3;                           // TMEM lane quadrant
     const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);
-    int it = 0;
+    uint8_t* stg = sEpi + q * 2 * 2048;
+    int it = 0, nstore = 0;
     for (int t = pair; t < num_tiles; t += npairs, ++it) {
       const int mb2 = t % num_m2, nb = t / num_m2;
       ptx::mbar_wait(ptx::smem_u32(tfull), it & 1, 24, it, t);
       ptx::tc_fence_after();
-      const int64_t row = (int64_t)mb2 * 256 + 128 * rank + q * 32 + lane;
-      const int64_t n0 = (int64_t)nb * 256;
+      const int row0 = mb2 * 256 + 128 * (int)rank + q * 32;
+      const int n0 = nb * 256;
 #pragma unroll 1
       for (int c = 0; c < 8; ++c) {
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + 32 * c, r);
         ptx::tc_wait_ld();
-        if (row < M) {
-          uint16_t* yrow = p.y + row * p.ldy + n0 + 32 * c;
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            if (n0 + 32 * c + 8 * v < N) {
-              uint4 o;
-              o.x = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
-              o.y = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
-              o.z = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
-              o.w = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
-              *reinterpret_cast<uint4*>(yrow + 8 * v) = o;
-            }
-          }
+        if (c == 7) {  // whole accumulator now in registers / stores: hand TMEM back
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
         }
+        if (p.dbg & 4) continue;
+        uint32_t w[16];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) w[v] = ptx::pack_bf16x2(__uint_as_float(r[2 * v]), __uint_as_float(r[2 * v + 1]));
+        uint8_t* buf = stg + (nstore & 1) * 2048;
+        if (lane == 0) ptx::bulk_wait_group_read<1>();   // the store that last used `buf` has read it
+        __syncwarp();
+        // row `lane` = 64 B in the TMA 64-byte swizzle layout (16-byte chunk k of row
+        // r at chunk k ^ ((r >> 1) & 3)): conflict-free, and w[] is indexed statically
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) =
+              make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_2d(&ty, ptx::smem_u32(buf), n0 + 32 * c, row0);
+          ptx::bulk_commit_group();
+        }
+        ++nstore;
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
     }
+    if (lane == 0) ptx::bulk_wait_group_read<0>();
   }
 
   ptx::tc_fence_before();
@@ -276,8 +315,8 @@ bool make_sf_map(CUtensorMap* m, const void* base, int64_t rows, int kp, int box
 }
 
 template <int STAGES>
-cudaError_t run2(const GemmArgs& a, cudaStream_t s, int64_t* launches, const char** err) {
-  CUtensorMap maps[12];
+cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches, const char** err) {
+  CUtensorMap maps[13];
   int first = -1;
   for (int g = 0; g < 3; ++g) {
     if (a.geom.n[g] == 0) continue;
@@ -295,6 +334,19 @@ cudaError_t run2(const GemmArgs& a, cudaStream_t s, int64_t* launches, const cha
   for (int g = 0; g < 3; ++g)
     if (a.geom.n[g] == 0)
       for (int k = 0; k < 4; ++k) maps[3 * k + g] = maps[3 * k + first];   // valid, never used
+  {  // Y [M, N] BF16 row-major (ld = ldy): TMA store boxes of 32 rows x 32 columns
+    EncodeTiledFn enc = tensor_map_encoder();
+    cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
+    cuuint64_t strides[1] = {(cuuint64_t)a.ldy * 2};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    if (!enc || enc(&maps[12], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, a.y, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      *err = "cuTensorMapEncodeTiled(Y) failed";
+      return cudaErrorInvalidValue;
+    }
+  }
   Gemm2Dev p{};
   p.M = a.M;
   p.N = a.N;
@@ -311,15 +363,17 @@ cudaError_t run2(const GemmArgs& a, cudaStream_t s, int64_t* launches, const cha
   p.idesc2 = make_idesc_mn(a.geom.fmt[2], 2, 256, 256);
   p.y = a.y;
   p.ldy = a.ldy;
+  { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   if (p.num_tiles == 0) return cudaSuccess;
-  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + (2 * STAGES + 2) * 8 + 16;
+  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + EPI_BYTES + (2 * STAGES + 2) * 8 + 16;
   auto kern = mixgemm2_kernel<STAGES>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
   int grid = sm_count() & ~1;
+  if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas & ~1;
   if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
   kern<<<grid, kThreads2, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7],
-                                     maps[8], maps[9], maps[10], maps[11], p);
+                                     maps[8], maps[9], maps[10], maps[11], maps[12], p);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
@@ -328,8 +382,8 @@ cudaError_t run2(const GemmArgs& a, cudaStream_t s, int64_t* launches, const cha
 
 cudaError_t launch_mixed_gemm_2cta(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
                                    const char** err) {
-  if (cfg.num_stages == 5) return run2<5>(a, s, launches, err);
-  return run2<6>(a, s, launches, err);
+  if (cfg.num_stages == 4) return run2<4>(a, cfg, s, launches, err);
+  return run2<5>(a, cfg, s, launches, err);
 }
 
 }  // namespace mmx

@@ -241,5 +241,89 @@ __device__ __forceinline__ void tc_mma_mxf4_cg2(uint32_t d, uint64_t adesc, uint
       : "memory");
 }
 
+// ---- whole-stage issue blocks for the CTA-pair GEMM ---------------------------------
+// Executed by a full, converged warp: elect.sync picks the single issuing lane, so
+// all operands stay warp-uniform (no per-instruction lane loops).  One FP8/FP6
+// stage: 3 scale-atom copies (SFA, SFB row groups 0/1) + 4 MMAs (K = 32 each,
+// scale-factor ids 0..3) + a commit that frees the smem stage in both CTAs.
+__device__ __forceinline__ void stage_f8f6_cg2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id0, uint32_t sfa,
+                                               uint32_t sfb, uint64_t sda, uint64_t sdb0, uint64_t sdb1,
+                                               uint32_t accum, uint32_t empty_bar) {
+  const uint32_t sfb4 = sfb + 4;
+  const uint32_t id1 = id0 | (1u << 29) | (1u << 4), id2 = id0 | (2u << 29) | (2u << 4), id3 = id0 | (3u << 29) | (3u << 4);
+  asm volatile(
+      "{\n\t.reg .pred p, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 acc, %9, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%4], %6;\n\t"
+      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%5], %7;\n\t"
+      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%13], %8;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%5], acc;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a1, b1, %10, [%4], [%5], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a2, b2, %11, [%4], [%5], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a3, b3, %12, [%4], [%5], one;\n\t"
+      "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%14], %15;\n\t}"
+      ::"r"(d), "l"(ad), "l"(bd), "r"(id0), "r"(sfa), "r"(sfb), "l"(sda), "l"(sdb0), "l"(sdb1), "r"(accum),
+        "r"(id1), "r"(id2), "r"(id3), "r"(sfb4), "r"(empty_bar), "h"((uint16_t)3)
+      : "memory");
+}
+// One full FP4 stage: 2 atoms each of SFA and of SFB row groups 0/1 + 4
+// kind::mxf4 MMAs (K = 64; MMA k uses atom k/2, scale-factor ids 0/2) + commit.
+__device__ __forceinline__ void stage_f4_cg2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id0, uint32_t sfa,
+                                             uint32_t sfb, uint64_t sda, uint64_t sdb0, uint64_t sdb1,
+                                             uint32_t accum, uint32_t empty_bar) {
+  // SFA atoms at columns sfa, sfa+4; SFB (atom a, row group r) at sfb + (2a + r) * 4
+  const uint32_t sfa4 = sfa + 4, sfb4 = sfb + 4, sfb8 = sfb + 8, sfb12 = sfb + 12;
+  const uint32_t id2 = id0 | (2u << 29) | (2u << 4);
+  asm volatile(
+      "{\n\t.reg .pred p, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3, sa1, s01, s11;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 acc, %9, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "add.s64 sa1, %6, 32;\n\tadd.s64 s01, %7, 32;\n\tadd.s64 s11, %8, 32;\n\t"
+      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%4], %6;\n\t"
+      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%11], sa1;\n\t"
+      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%5], %7;\n\t"
+      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%12], %8;\n\t"
+      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%13], s01;\n\t"
+      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%14], s11;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], acc;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a1, b1, %10, [%4], [%5], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a2, b2, %3, [%11], [%13], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a3, b3, %10, [%11], [%13], one;\n\t"
+      "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%15], %16;\n\t}"
+      ::"r"(d), "l"(ad), "l"(bd), "r"(id0), "r"(sfa), "r"(sfb), "l"(sda), "l"(sdb0), "l"(sdb1), "r"(accum),
+        "r"(id2), "r"(sfa4), "r"(sfb4), "r"(sfb8), "r"(sfb12), "r"(empty_bar), "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void commit_cg2_mc_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+      "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+      ::"r"(bar), "h"((uint16_t)3)
+      : "memory");
+}
+
+// ---- TMA stores -----------------------------------------------------------------
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const void* desc, uint32_t src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
 }  // namespace ptx
 }  // namespace mmx

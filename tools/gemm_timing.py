@@ -33,6 +33,8 @@ def time_gemm(M, N, n, reps=20):
 
 if __name__ == "__main__":
     M, N = int(sys.argv[1]), int(sys.argv[2])
+    mm.mm_set_gemm_config(int(os.environ.get("BN", "0")), int(os.environ.get("STAGES", "0")),
+                          int(os.environ.get("MAXCTAS", "0")))
     splits = [tuple(int(v) for v in a.split(",")) for a in sys.argv[3:]] or [
         (4096, 0, 0), (0, 4096, 0), (0, 0, 4096), (2240, 1184, 672)]
     for n in splits:
