@@ -30,12 +30,23 @@ namespace mmx {
 namespace {
 
 constexpr int kThreads2 = 256;
+// Timeline trace (env MM_GEMM_DEBUG & 32; read with mm_debug_gemm_trace): per CTA
+// [start, setup, first stage ready, tile0 start, tile0 issued, tile1 start, tile1
+// issued, tile2 start, tile2 issued, epi0 ready, epi1 ready, epi2 ready, epi done].
+__device__ unsigned long long g_trace[160][16];
 constexpr int A_BYTES = 128 * 128;       // this CTA's 128 rows x 128 B
 constexpr int B_BYTES = 128 * 128;       // this CTA's 128 W rows x 128 B
 constexpr int SFA_BYTES = 2 * 512;       // up to 2 atoms (FP4 stage)
 constexpr int SFB_BYTES = 2 * 2 * 512;   // 2 row groups (N = 256) x up to 2 atoms
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
-constexpr int SF_STRIDE = 24;            // TMEM columns per stage: SFA 2x4, SFB 2x2x4
+constexpr int SF_STRIDE = 24;            // TMEM columns per scale slot: SFA 2x4, SFB 2x2x4
+// TMEM (512 columns): two 256-column accumulators that OVERLAP by 48 columns,
+// acc0 = [0, 256), acc1 = [208, 464), and two scale slots in [464, 512).  The
+// epilogue drains the overlapping columns of an accumulator first and releases them
+// early, so the next tile's MMAs (into the other accumulator) start after ~1/4 of
+// the epilogue instead of after all of it.
+constexpr int ACC1_COL = 208;
+constexpr int SF_COL = 464;
 constexpr int EPI_BYTES = 4 * 2 * 32 * 64;  // epilogue staging: 4 warps x 2 buffers x (32 x 32 BF16)
 
 struct Gemm2Dev {
@@ -86,12 +97,15 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_BYTES);
   uint64_t* full = bars;                  // [STAGES]  (used in the even CTA)
   uint64_t* empty = bars + STAGES;        // [STAGES]  (each CTA)
-  uint64_t* tfull = bars + 2 * STAGES;    // [1]       (each CTA)
-  uint64_t* tempty = tfull + 1;           // [1]       (even CTA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tfull = bars + 2 * STAGES;    // [2] per accumulator (each CTA)
+  uint64_t* tempty = tfull + 2;           // [2] accumulator fully drained (even CTA)
+  uint64_t* tovl = tempty + 2;            // [2] overlap columns drained (even CTA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tovl + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();    // 0 = MMA leader
+  const uint64_t t_start = ptx::globaltimer_ns();
+  const bool trace = (p.dbg & 32) && lane == 0;
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
 
   if (warp == 0 && lane == 0) {
@@ -105,8 +119,11 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&empty[i]), 1);
     }
-    ptx::mbar_init(ptx::smem_u32(tfull), 1);
-    ptx::mbar_init(ptx::smem_u32(tempty), 8);     // 4 epilogue warps x 2 CTAs
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&tfull[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&tempty[i]), 8);   // 4 epilogue warps x 2 CTAs
+      ptx::mbar_init(ptx::smem_u32(&tovl[i]), 8);
+    }
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), 512);
@@ -114,6 +131,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::grid_dep_launch();
+  ptx::grid_dep_wait();   // A, W, scales may come from the preceding kernel; Y may still be read by it
+  if (trace && warp == 1) { g_trace[blockIdx.x][0] = t_start; g_trace[blockIdx.x][1] = ptx::globaltimer_ns(); }
   const int64_t M = p.M, N = p.N;
   const int num_m2 = p.num_m2, num_tiles = p.num_tiles;
 
@@ -184,7 +204,12 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       const uint32_t empty0 = ptx::smem_u32(&empty[0]), full0 = ptx::smem_u32(&full[0]);
       const bool no_mma = (p.dbg & 2) != 0;
       for (int t = pair; t < num_tiles; t += npairs, ++it) {
-        ptx::mbar_wait(ptx::smem_u32(tempty), (it & 1) ^ 1, 22, it, t);
+        const int acc = it & 1;
+        const uint32_t d_t = tmem_base + (acc ? ACC1_COL : 0);
+        ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), ((it >> 1) & 1) ^ 1, 22, it, t);   // tile it-2 drained acc
+        if (it > 0) ptx::mbar_wait(ptx::smem_u32(&tovl[acc ^ 1]), ((it - 1) >> 1) & 1, 25, it, t);  // overlap of it-1
+        if (trace && it < 3) g_trace[blockIdx.x][3 + 2 * it] = ptx::globaltimer_ns();
+        if (trace && it == 0) g_trace[blockIdx.x][13] = clock64();
         ptx::tc_fence_after();
         uint32_t accum = 0;
 #pragma unroll
@@ -197,8 +222,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
           for (int j = 0; j < nst; ++j) {
             const int nmma = min((n_g - kstage * j + kmma - 1) / kmma, 4);
             ptx::mbar_wait(full0 + 8 * stage, phase, 23, stage, t);
+            if (trace && it == 0 && g == 0 && j == 0) g_trace[blockIdx.x][2] = ptx::globaltimer_ns();
             ptx::tc_fence_after();
-            const uint32_t sfa_t = tmem_base + 256 + stage * SF_STRIDE;
+            const uint32_t sfa_t = tmem_base + SF_COL + (stage & 1) * SF_STRIDE;
             const uint32_t sfb_t = sfa_t + 8;
             const uint64_t ad = ptx::smem_desc(sA0 + stage * A_BYTES, 16, 1024, 2);
             const uint64_t bd = ptx::smem_desc(sB0 + stage * B_BYTES, 16, 1024, 2);
@@ -206,8 +232,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
             const uint64_t sdb0 = ptx::smem_desc(sSFB0 + stage * SFB_BYTES, 0, 128, 0);
             const uint64_t sdb1 = ptx::smem_desc(sSFB0 + stage * SFB_BYTES + 1024, 0, 128, 0);
             if (nmma == 4 && !no_mma) {
-              if (g == 0) ptx::stage_f4_cg2(tmem_base, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage);
-              else ptx::stage_f8f6_cg2(tmem_base, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage);
+              if (g == 0) ptx::stage_f4_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage);
+              else ptx::stage_f8f6_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage,
+                                       (p.dbg & 64) ? 0u : 1u);
               accum = 1;
             } else {
               // partial stage: scale copies for the atoms it uses, then nmma MMAs
@@ -221,10 +248,10 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
                 for (int k = 0; k < (no_mma ? 0 : nmma); ++k) {
                   if (g == 0) {
                     const uint32_t sid = 2u * (k & 1);
-                    ptx::tc_mma_mxf4_cg2(tmem_base, ad + 2 * k, bd + 2 * k, idesc | (sid << 29) | (sid << 4),
+                    ptx::tc_mma_mxf4_cg2(d_t, ad + 2 * k, bd + 2 * k, idesc | (sid << 29) | (sid << 4),
                                          sfa_t + 4 * (k >> 1), sfb_t + (k >> 1) * 8, accum);
                   } else {
-                    ptx::tc_mma_mxf8f6f4_cg2(tmem_base, ad + 2 * k, bd + 2 * k, idesc | ((uint32_t)k << 29) | ((uint32_t)k << 4),
+                    ptx::tc_mma_mxf8f6f4_cg2(d_t, ad + 2 * k, bd + 2 * k, idesc | ((uint32_t)k << 29) | ((uint32_t)k << 4),
                                              sfa_t, sfb_t, accum);
                   }
                   accum = 1;
@@ -237,7 +264,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }
-        ptx::commit_cg2_mc_elect(ptx::smem_u32(tfull));
+        ptx::commit_cg2_mc_elect(ptx::smem_u32(&tfull[acc]));
+        if (trace && it < 3) g_trace[blockIdx.x][4 + 2 * it] = ptx::globaltimer_ns();
+        if (trace && it == 0) g_trace[blockIdx.x][14] = clock64();
         __syncwarp();
       }
     }
@@ -249,24 +278,31 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     // chunk's conversion overlap the previous store; the accumulator is released to
     // the MMA warp as soon as its last chunk is in registers.
     const int q = warp & 3;                           // TMEM lane quadrant
-    const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);
+    const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
+    const uint32_t tovl_leader = ptx::mapa(ptx::smem_u32(&tovl[0]), 0);
     uint8_t* stg = sEpi + q * 2 * 2048;
     int it = 0, nstore = 0;
     for (int t = pair; t < num_tiles; t += npairs, ++it) {
       const int mb2 = t % num_m2, nb = t / num_m2;
-      ptx::mbar_wait(ptx::smem_u32(tfull), it & 1, 24, it, t);
+      const int acc = it & 1;
+      ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), (it >> 1) & 1, 24, it, t);
+      if (trace && q == 0 && it < 3) g_trace[blockIdx.x][9 + it] = ptx::globaltimer_ns();
       ptx::tc_fence_after();
       const int row0 = mb2 * 256 + 128 * (int)rank + q * 32;
       const int n0 = nb * 256;
+      const uint32_t acc_col = acc ? ACC1_COL : 0;
 #pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
+      for (int i = 0; i < 8; ++i) {
+        // acc0: its overlap (columns 208..255) lives in chunks 6, 7 -> drain those first;
+        // acc1: its overlap is its own columns 0..47 -> chunks 0, 1 come first anyway.
+        const int c = acc ? i : (i + 6) & 7;
         uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + 32 * c, r);
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc_col + 32 * c, r);
         ptx::tc_wait_ld();
-        if (c == 7) {  // whole accumulator now in registers / stores: hand TMEM back
+        if (i == 1 || i == 7) {  // overlap drained / whole accumulator drained
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
+          if (lane == 0) ptx::mbar_arrive_cluster((i == 1 ? tovl_leader : tempty_leader) + 8 * acc);
         }
         if (p.dbg & 4) continue;
         uint32_t w[16];
@@ -291,6 +327,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       }
     }
     if (lane == 0) ptx::bulk_wait_group_read<0>();
+    if (trace && q == 0) g_trace[blockIdx.x][12] = ptx::globaltimer_ns();
   }
 
   ptx::tc_fence_before();
@@ -365,20 +402,28 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.ldy = a.ldy;
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   if (p.num_tiles == 0) return cudaSuccess;
-  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + EPI_BYTES + (2 * STAGES + 2) * 8 + 16;
+  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + EPI_BYTES + (2 * STAGES + 6) * 8 + 16;
   auto kern = mixgemm2_kernel<STAGES>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
   int grid = sm_count() & ~1;
   if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas & ~1;
   if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
-  kern<<<grid, kThreads2, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7],
-                                     maps[8], maps[9], maps[10], maps[11], maps[12], p);
+  e = launch_pdl(kern, dim3(grid), dim3(kThreads2), smem, s, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
+                 maps[6], maps[7], maps[8], maps[9], maps[10], maps[11], maps[12], p);
   if (launches) ++*launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace
+}  // namespace mmx
+
+// Debug hook (not part of include/mm.h): copy the GEMM timeline trace to the host.
+extern "C" int mm_debug_gemm_trace(unsigned long long* h, int n) {
+  return (int)cudaMemcpyFromSymbol(h, mmx::g_trace, sizeof(unsigned long long) * (size_t)(n < 2560 ? n : 2560));
+}
+
+namespace mmx {
 
 cudaError_t launch_mixed_gemm_2cta(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
                                    const char** err) {

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 namespace mmx {
 
@@ -90,6 +92,25 @@ cudaError_t launch_mixed_gemm_2cta(const GemmArgs& a, const GemmConfig& cfg, cud
 // shared-memory limit once, and remember occupancy queries, so the hot calls do
 // no redundant driver work per launch.
 cudaError_t ensure_smem_attr(const void* func, size_t smem);
+
+// Launch with programmatic stream serialization (PDL): the kernel's prologue
+// overlaps the tail of the preceding kernel; the kernel itself calls
+// griddepcontrol.wait before touching dependent memory.  MM_NO_PDL=1 disables it.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  static const bool no_pdl = [] { const char* e = getenv("MM_NO_PDL"); return e && atoi(e); }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 cudaError_t cached_occupancy(const void* func, int threads, size_t smem, int* per_sm);
 
 // NCCL entry points resolved with dlopen (comm.cu).

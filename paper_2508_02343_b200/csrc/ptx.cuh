@@ -176,6 +176,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
+// ---- programmatic dependent launch ----------------------------------------------
+// wait: block until the preceding grid in the stream has completed and its memory
+// is visible (call before touching anything it may produce or still read);
+// launch_dependents: allow the next grid to be scheduled as SMs free up.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- clusters / CTA pairs ------------------------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -248,26 +255,27 @@ __device__ __forceinline__ void tc_mma_mxf4_cg2(uint32_t d, uint64_t adesc, uint
 // scale-factor ids 0..3) + a commit that frees the smem stage in both CTAs.
 __device__ __forceinline__ void stage_f8f6_cg2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id0, uint32_t sfa,
                                                uint32_t sfb, uint64_t sda, uint64_t sdb0, uint64_t sdb1,
-                                               uint32_t accum, uint32_t empty_bar) {
+                                               uint32_t accum, uint32_t empty_bar, uint32_t do_cp = 1) {
   const uint32_t sfb4 = sfb + 4;
   const uint32_t id1 = id0 | (1u << 29) | (1u << 4), id2 = id0 | (2u << 29) | (2u << 4), id3 = id0 | (3u << 29) | (3u << 4);
   asm volatile(
-      "{\n\t.reg .pred p, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "{\n\t.reg .pred p, acc, one, c;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
       "setp.ne.b32 acc, %9, 0;\n\t"
       "setp.eq.b32 one, 0, 0;\n\t"
+      "setp.ne.and.b32 c, %16, 0, p;\n\t"
       "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
       "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
-      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%4], %6;\n\t"
-      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%5], %7;\n\t"
-      "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%13], %8;\n\t"
+      "@c tcgen05.cp.cta_group::2.32x128b.warpx4 [%4], %6;\n\t"
+      "@c tcgen05.cp.cta_group::2.32x128b.warpx4 [%5], %7;\n\t"
+      "@c tcgen05.cp.cta_group::2.32x128b.warpx4 [%13], %8;\n\t"
       "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%5], acc;\n\t"
       "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a1, b1, %10, [%4], [%5], one;\n\t"
       "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a2, b2, %11, [%4], [%5], one;\n\t"
       "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a3, b3, %12, [%4], [%5], one;\n\t"
       "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%14], %15;\n\t}"
       ::"r"(d), "l"(ad), "l"(bd), "r"(id0), "r"(sfa), "r"(sfb), "l"(sda), "l"(sdb0), "l"(sdb1), "r"(accum),
-        "r"(id1), "r"(id2), "r"(id3), "r"(sfb4), "r"(empty_bar), "h"((uint16_t)3)
+        "r"(id1), "r"(id2), "r"(id3), "r"(sfb4), "r"(empty_bar), "h"((uint16_t)3), "r"(do_cp)
       : "memory");
 }
 // One full FP4 stage: 2 atoms each of SFA and of SFB row groups 0/1 + 4

@@ -131,36 +131,45 @@ __device__ __forceinline__ void scaled8(const ST* v, float inv, float (&f)[8]) {
   }
 }
 
-// Encode + store row RHO of one 32-element block (v = the 32 gathered two-row
-// slots) for segment kind G (0 FP4, 1 FP6, 2 FP8) in element format FMT.
-template <int G, int FMT, int RHO, typename ST>
-__device__ __forceinline__ void encode_store(const ST (&v)[32], float inv, uint8_t* dst) {
-  if constexpr (G == 0) {  // MXFP4: 16 bytes
-    uint32_t w[4];
+// Encode + store row RHO of NV consecutive channels of one 32-element block (NV =
+// 32: the whole block; NV = 16: one half, the lane pair splits the block) for
+// segment kind G (0 FP4, 1 FP6, 2 FP8) in element format FMT.
+template <int G, int FMT, int RHO, int NV, typename ST>
+__device__ __forceinline__ void encode_store(const ST (&v)[NV], float inv, uint8_t* dst) {
+  if constexpr (G == 0) {  // MXFP4: NV/2 bytes
+    uint32_t w[NV / 8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NV / 8; ++q) {
       float f[8];
       scaled8<RHO>(v + 8 * q, inv, f);
       w[q] = cvt_e2m1_x8(f);
     }
-    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-  } else if constexpr (G == 1) {  // MXFP6: 24 bytes, LSB-first 6-bit stream
-    uint32_t q24[8];
+    if constexpr (NV == 32) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    else *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+  } else if constexpr (G == 1) {  // MXFP6: 3 NV / 4 bytes, LSB-first 6-bit stream
+    uint32_t q24[NV / 4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NV / 8; ++q) {
       float f[8];
       scaled8<RHO>(v + 8 * q, inv, f);
       q24[2 * q] = Cvt<FMT>::x4(f[0], f[1], f[2], f[3]);
       q24[2 * q + 1] = Cvt<FMT>::x4(f[4], f[5], f[6], f[7]);
     }
-    uint2* d2 = reinterpret_cast<uint2*>(dst);
-    d2[0] = make_uint2(q24[0] | (q24[1] << 24), (q24[1] >> 8) | (q24[2] << 16));
-    d2[1] = make_uint2((q24[2] >> 16) | (q24[3] << 8), q24[4] | (q24[5] << 24));
-    d2[2] = make_uint2((q24[5] >> 8) | (q24[6] << 16), (q24[6] >> 16) | (q24[7] << 8));
-  } else {  // MXFP8: 32 bytes
-    uint32_t w[8];
+    if constexpr (NV == 32) {
+      uint2* d2 = reinterpret_cast<uint2*>(dst);
+      d2[0] = make_uint2(q24[0] | (q24[1] << 24), (q24[1] >> 8) | (q24[2] << 16));
+      d2[1] = make_uint2((q24[2] >> 16) | (q24[3] << 8), q24[4] | (q24[5] << 24));
+      d2[2] = make_uint2((q24[5] >> 8) | (q24[6] << 16), (q24[6] >> 16) | (q24[7] << 8));
+    } else {  // 12 bytes, 4-byte aligned
+      uint32_t* d1 = reinterpret_cast<uint32_t*>(dst);
+      d1[0] = q24[0] | (q24[1] << 24);
+      d1[1] = (q24[1] >> 8) | (q24[2] << 16);
+      d1[2] = (q24[2] >> 16) | (q24[3] << 8);
+    }
+  } else {  // MXFP8: NV bytes
+    uint32_t w[NV / 4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NV / 8; ++q) {
       float f[8];
       scaled8<RHO>(v + 8 * q, inv, f);
       w[2 * q] = Cvt<FMT>::x4(f[0], f[1], f[2], f[3]);
@@ -168,30 +177,40 @@ __device__ __forceinline__ void encode_store(const ST (&v)[32], float inv, uint8
     }
     uint4* d4 = reinterpret_cast<uint4*>(dst);
     d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
-    d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    if constexpr (NV == 32) d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
 }
 
-// Block amax of each of the R rows over |bf16| bits (packed 16x2 maxima).
-__device__ __forceinline__ void block_amax(const uint16_t (&v)[32], uint32_t (&am)[4]) {
+// Block amax of each of the R rows over |bf16| bits (packed 16x2 maxima).  With
+// NV = 16 each lane holds half a block; the lane pair combines with one shuffle.
+template <int NV>
+__device__ __forceinline__ void block_amax(const uint16_t (&v)[NV], uint32_t (&am)[4]) {
   uint32_t m = 0;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) m = max(m, uint32_t(v[i]) & 0x7FFFu);
+  for (int i = 0; i < NV; ++i) m = max(m, uint32_t(v[i]) & 0x7FFFu);
+  if constexpr (NV == 16) m = max(m, __shfl_xor_sync(3u << (threadIdx.x & 30), m, 1));
   am[0] = m;
 }
-__device__ __forceinline__ void block_amax(const uint32_t (&v)[32], uint32_t (&am)[4]) {
+template <int NV>
+__device__ __forceinline__ void block_amax(const uint32_t (&v)[NV], uint32_t (&am)[4]) {
   uint32_t m = 0;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) m = __vmaxu2(m, v[i] & 0x7FFF7FFFu);
+  for (int i = 0; i < NV; ++i) m = __vmaxu2(m, v[i] & 0x7FFF7FFFu);
+  if constexpr (NV == 16) m = __vmaxu2(m, __shfl_xor_sync(3u << (threadIdx.x & 30), m, 1));
   am[0] = m & 0xFFFFu;
   am[1] = m >> 16;
 }
-__device__ __forceinline__ void block_amax(const uint2 (&v)[32], uint32_t (&am)[4]) {
+template <int NV>
+__device__ __forceinline__ void block_amax(const uint2 (&v)[NV], uint32_t (&am)[4]) {
   uint32_t m01 = 0, m23 = 0;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < NV; ++i) {
     m01 = __vmaxu2(m01, v[i].x & 0x7FFF7FFFu);
     m23 = __vmaxu2(m23, v[i].y & 0x7FFF7FFFu);
+  }
+  if constexpr (NV == 16) {
+    m01 = __vmaxu2(m01, __shfl_xor_sync(3u << (threadIdx.x & 30), m01, 1));
+    m23 = __vmaxu2(m23, __shfl_xor_sync(3u << (threadIdx.x & 30), m23, 1));
   }
   am[0] = m01 & 0xFFFFu;
   am[1] = m01 >> 16;
@@ -202,28 +221,33 @@ __device__ __forceinline__ void block_amax(const uint2 (&v)[32], uint32_t (&am)[
 // One row of one block: E8M0 exponent by integer arithmetic on the BF16 exponent
 // field (e = floor(log2 amax) - off, clamped at -127; zero and subnormal amax give
 // -127), the scale byte into its 128x4 atom (rows of a tile are consecutive rows of
-// one 32-row group: +16 bytes per row), codes packed and stored.
-template <int RHO, int G, int FMT, typename ST>
-__device__ __forceinline__ void quantize_row(const ST (&v)[32], uint32_t amax, int off, uint8_t* crow,
-                                             uint8_t* sfp, bool store_codes) {
+// one 32-row group: +16 bytes per row; written by the even lane of a pair), codes
+// packed and stored.
+template <int RHO, int G, int FMT, int NV, typename ST>
+__device__ __forceinline__ void quantize_row(const ST (&v)[NV], uint32_t amax, int off, uint8_t* crow,
+                                             uint8_t* sfp, bool store_codes, bool store_sf) {
   const int sb = max(int(amax >> 7) - off, 0);                  // E8M0 byte = e + 127
   const float inv = __uint_as_float(uint32_t(254 - sb) << 23);  // 2^-e exactly
-  sfp[16 * RHO] = uint8_t(sb);
-  if (store_codes) encode_store<G, FMT, RHO>(v, inv, crow);
+  if (store_sf) sfp[16 * RHO] = uint8_t(sb);
+  if (store_codes) encode_store<G, FMT, RHO, NV>(v, inv, crow);
 }
 
-template <int R, int G, int FMT>
-__device__ __forceinline__ void quantize_tile_block(const typename Slot<R>::T (&v)[32], int off, uint8_t* crow0,
-                                                    int64_t pitch, uint8_t* sfp, int nvalid) {
+template <int R, int G, int FMT, int NV>
+__device__ __forceinline__ void quantize_tile_block(const typename Slot<R>::T (&v)[NV], int off, uint8_t* crow0,
+                                                    int64_t pitch, uint8_t* sfp, int nvalid, bool store_sf) {
   uint32_t am[4];
-  block_amax(v, am);
-  quantize_row<0, G, FMT>(v, am[0], off, crow0, sfp, nvalid > 0);
-  if constexpr (R >= 2) quantize_row<1, G, FMT>(v, am[1], off, crow0 + pitch, sfp, nvalid > 1);
+  block_amax<NV>(v, am);
+  quantize_row<0, G, FMT, NV>(v, am[0], off, crow0, sfp, nvalid > 0, store_sf);
+  if constexpr (R >= 2) quantize_row<1, G, FMT, NV>(v, am[1], off, crow0 + pitch, sfp, nvalid > 1, store_sf);
   if constexpr (R >= 4) {
-    quantize_row<2, G, FMT>(v, am[2], off, crow0 + 2 * pitch, sfp, nvalid > 2);
-    quantize_row<3, G, FMT>(v, am[3], off, crow0 + 3 * pitch, sfp, nvalid > 3);
+    quantize_row<2, G, FMT, NV>(v, am[2], off, crow0 + 2 * pitch, sfp, nvalid > 2, store_sf);
+    quantize_row<3, G, FMT, NV>(v, am[3], off, crow0 + 3 * pitch, sfp, nvalid > 3, store_sf);
   }
 }
+
+// Timeline trace (env MM_RQ_DEBUG & 32; read with mm_debug_rq_trace): per CTA
+// [start, table ready, tile0 data ready, tile0 done, tile1 ready, tile1 done, ..., last TMA issued].
+__device__ unsigned long long g_rq_trace[160][16];
 
 struct RqDev {
   RqArgs a;
@@ -249,7 +273,7 @@ struct RqDev {
 //    16-byte vectors), block amax, scale and encode as above; finally the stage
 //    is released to the producer.
 template <int R>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(704, 1)
 rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev d) {
   using ST = typename Slot<R>::T;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -259,14 +283,16 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   const RqArgs& a = d.a;
   const int stage_bytes = d.nbox * 512 * R;
   // [ring of stages][perm copy: K x int32][gather table: K x u16][barriers]
-  const int K = a.K, nblk = K / 32;
-  const size_t tab_bytes = d.perm_smem ? (size_t)K * 6 : 0;
+  const int K = a.K, nblk = K / 32, nblk_s = nblk + 1;   // table row stride padded (bank spread)
+  const size_t tab_bytes = d.perm_smem ? (size_t)K * 4 + (size_t)16 * (K / 32 + 1) * 4 : 0;
   const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
-  uint32_t* gidx = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + (size_t)K * 4);
+  uint32_t* gidx = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + (size_t)K * 4);   // 16 x nblk_s words
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)d.stages * stage_bytes + tab_bytes);
   uint64_t* empty = full + d.stages;
   uint64_t* permbar = empty + d.stages;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint64_t t_start = ptx::globaltimer_ns();
+  if (threadIdx.x == 0 && (d.dbg & 32)) g_rq_trace[blockIdx.x][0] = t_start;
   if (threadIdx.x == 0) {
     for (int i = 0; i < d.stages; ++i) {
       ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
@@ -283,8 +309,10 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   __syncthreads();
   const int64_t my_tiles = (d.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
+  ptx::grid_dep_launch();
   if (warp == 0) {
     // ============================ TMA producer ============================
+    ptx::grid_dep_wait();   // X may be produced by the preceding kernel
     if (lane == 0) {
       const uint32_t tx = (uint32_t)stage_bytes;
       for (int64_t i = 0; i < my_tiles; ++i) {
@@ -299,6 +327,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
         if (d.box3d) ptx::tma_load_3d(dst, &tmx, fb, 0, row0, 0);   // all boxes of the tile at once
         else
           for (int b = 0; b < d.nbox; ++b) ptx::tma_load_2d(dst + b * 512 * R, &tmx, fb, 256 * b, row0);
+        if ((d.dbg & 32) && i == my_tiles - 1) g_rq_trace[blockIdx.x][14] = ptx::globaltimer_ns();
       }
     }
     return;
@@ -333,19 +362,23 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     for (int t = ct; t < K / 2; t += cn) {
       const int blk = t >> 4, i2 = t & 15;
       const uint2 pr = *reinterpret_cast<const uint2*>(perm_s + 32 * blk + 2 * i2);
-      gidx[i2 * nblk + blk] = pr.x | (pr.y << 16);
+      gidx[i2 * nblk_s + blk] = pr.x | (pr.y << 16);
     }
     ptx::named_bar_sync(15, cn);
+    if ((d.dbg & 32) && threadIdx.x == 32) g_rq_trace[blockIdx.x][1] = ptx::globaltimer_ns();
   }
-  // Work is split into chunks of 32 consecutive blocks of ONE segment (a warp's
-  // lanes never mix segments, so the encode path is warp-uniform).
-  const int nch0 = (kp0 / 32 + 31) / 32, nch1 = (kp1 / 32 + 31) / 32, nch2 = (kp2 / 32 + 31) / 32;
+  ptx::grid_dep_wait();   // the outputs may still be read by the preceding kernel
+  // Work is split into chunks of 16 consecutive blocks of ONE segment (a warp's
+  // lanes never mix segments, so the encode path is warp-uniform); the two lanes of
+  // a pair share a block, 16 channels each.
+  const int nch0 = (kp0 / 32 + 15) / 16, nch1 = (kp1 / 32 + 15) / 16, nch2 = (kp2 / 32 + 15) / 16;
   const int nch = nch0 + nch1 + nch2;
   for (int64_t i = grp; i < my_tiles; i += groups) {
     const int s = int(i % stages);
     const uint32_t ph = uint32_t(i / stages) & 1u;
     uint8_t* st = smem + (size_t)s * stage_bytes;
     ptx::mbar_wait(ptx::smem_u32(&full[s]), ph, 12, s, (int)i);
+    if ((d.dbg & 32) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][2 + 2 * i] = ptx::globaltimer_ns();
     // ---- in-place transpose: box [R rows][256] -> 256 slots of R values ----
     if constexpr (R > 1) {
       for (int b = gw; b < nbox && dbg < 2; b += group_warps) {
@@ -380,11 +413,12 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     const int64_t r0 = (blockIdx.x + i * gridDim.x) * (int64_t)R;
     const int64_t left = rows - r0;
     const int nvalid = left >= R ? R : (left > 0 ? (int)left : 0);
+    const int h = lane & 1;                      // which half of the block
     for (int ch = gw; ch < nch; ch += group_warps) {
       const int g = ch < nch0 ? 0 : (ch < nch0 + nch1 ? 1 : 2);
-      const int kb = (ch - (g == 0 ? 0 : (g == 1 ? nch0 : nch0 + nch1))) * 32 + lane;
+      const int kb = (ch - (g == 0 ? 0 : (g == 1 ? nch0 : nch0 + nch1))) * 16 + (lane >> 1);
       const int kp_g = g == 0 ? kp0 : (g == 1 ? kp1 : kp2);
-      if (kb >= kp_g / 32) continue;
+      if (kb >= kp_g / 32) continue;             // pair-uniform
       const int n_g = g == 0 ? n0 : (g == 1 ? n1 : n2);
       const int off_g = g == 0 ? of0 : (g == 1 ? of1 : of2);
       const int fmt = g == 1 ? fm1 : fm2;
@@ -393,31 +427,32 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       uint8_t* sf_g = g == 0 ? sf0 : (g == 1 ? sf1 : sf2);
       uint8_t* codes_g = g == 0 ? cd0 : (g == 1 ? cd1 : cd2);
       uint8_t* sfp = sf_g + sf_offset(r0, kb, kp_g / 128);
-      const int bpb = g == 0 ? 16 : (g == 1 ? 24 : 32);
-      uint8_t* crow0 = codes_g + r0 * pitch + (int64_t)kb * bpb;
-      if (kb * 32 >= n_g) {
+      const int hb = g == 0 ? 8 : (g == 1 ? 12 : 16);   // code bytes per half block
+      uint8_t* crow0 = codes_g + r0 * pitch + (int64_t)kb * 2 * hb + h * hb;
+      if (kb * 32 >= n_g || (dbg & 8)) {   // dbg 8: timing experiment, stores only
         // padding block: zero codes and zero scale bytes
+        if (dbg & 16) continue;             // timing experiment: no stores at all
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) {
-          sfp[16 * rho] = 0;
+          if (h == 0) sfp[16 * rho] = 0;
           if (rho < nvalid)
-            for (int b = 0; b < bpb; b += 8) *reinterpret_cast<uint2*>(crow0 + rho * pitch + b) = make_uint2(0, 0);
+            for (int b = 0; b < hb; b += 4) *reinterpret_cast<uint32_t*>(crow0 + rho * pitch + b) = 0u;
         }
         continue;
       }
-      ST v[32];
+      ST v[16];
       if (use_tab) {
-        const uint32_t* gp = gidx + off_g / 32 + kb;
+        const uint32_t* gp = gidx + (off_g / 32 + kb) + 8 * h * nblk_s;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const uint32_t pr = gp[q * nblk];
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t pr = gp[q * nblk_s];
           v[2 * q + 0] = slots[pr & 0xFFFFu];
           v[2 * q + 1] = slots[pr >> 16];
         }
       } else {
-        const int4* pp = reinterpret_cast<const int4*>(a.perm + off_g + 32 * kb);
+        const int4* pp = reinterpret_cast<const int4*>(a.perm + off_g + 32 * kb + 16 * h);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
           const int4 pv = __ldg(pp + q);
           v[4 * q + 0] = slots[pv.x];
           v[4 * q + 1] = slots[pv.y];
@@ -425,15 +460,17 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
           v[4 * q + 3] = slots[pv.w];
         }
       }
-      if (g == 0) quantize_tile_block<R, 0, F_E2M1>(v, off, crow0, pitch, sfp, nvalid);
+      const bool sf_lane = h == 0;
+      if (g == 0) quantize_tile_block<R, 0, F_E2M1, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
       else if (g == 1) {
-        if (fmt == F_E3M2) quantize_tile_block<R, 1, F_E3M2>(v, off, crow0, pitch, sfp, nvalid);
-        else quantize_tile_block<R, 1, F_E2M3>(v, off, crow0, pitch, sfp, nvalid);
+        if (fmt == F_E3M2) quantize_tile_block<R, 1, F_E3M2, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
+        else quantize_tile_block<R, 1, F_E2M3, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
       } else {
-        if (fmt == F_E4M3) quantize_tile_block<R, 2, F_E4M3>(v, off, crow0, pitch, sfp, nvalid);
-        else quantize_tile_block<R, 2, F_E5M2>(v, off, crow0, pitch, sfp, nvalid);
+        if (fmt == F_E4M3) quantize_tile_block<R, 2, F_E4M3, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
+        else quantize_tile_block<R, 2, F_E5M2, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
       }
     }
+    if ((d.dbg & 32) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][3 + 2 * i] = ptx::globaltimer_ns();
     // ---- release the stage (every warp of the group arrives once) ----
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s]));
@@ -459,18 +496,19 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   d.nbox = (a.K + 255) / 256;
   const size_t stage_bytes = (size_t)d.nbox * 512 * R;
   // Stage the permutation in smem (gather table) when that still leaves >= 3 stages.
-  d.perm_smem = (200 * 1024 - (size_t)a.K * 6) / stage_bytes >= 3 ? 1 : 0;
-  const size_t tab_bytes = d.perm_smem ? (size_t)a.K * 6 : 0;
+  const size_t tab_need = (size_t)a.K * 4 + (size_t)16 * (a.K / 32 + 1) * 4;   // perm copy + gather table
+  d.perm_smem = (200 * 1024 - tab_need) / stage_bytes >= 3 ? 1 : 0;
+  const size_t tab_bytes = d.perm_smem ? tab_need : 0;
   int stages = (int)((200 * 1024 - tab_bytes) / stage_bytes);
   if (stages > 8) stages = 8;
   { const char* e = getenv("MM_RQ_STAGES"); if (e && atoi(e) >= 2 && atoi(e) < stages) stages = atoi(e); }
   if (stages < 2) return cudaErrorInvalidConfiguration;
   d.stages = stages;
-  int gw = (a.geom.kp[0] / 32 + 31) / 32 + (a.geom.kp[1] / 32 + 31) / 32 + (a.geom.kp[2] / 32 + 31) / 32;
-  if (gw > 8) gw = 8;
+  int gw = (a.geom.kp[0] / 32 + 15) / 16 + (a.geom.kp[1] / 32 + 15) / 16 + (a.geom.kp[2] / 32 + 15) / 16;
+  if (gw > 12) gw = 12;
   if (gw < 2) gw = 2;
   d.group_warps = gw;
-  int groups = 15 / gw;   // <= 15 consumer warps + the producer warp
+  int groups = 21 / gw;   // <= 21 consumer warps + the producer warp (register budget)
   if (groups > stages - 1) groups = stages - 1;
   if (groups < 1) groups = 1;
   d.groups = groups;
@@ -507,9 +545,9 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   const int threads = 32 * (1 + groups * gw);
   int64_t grid = sm_count();
   if (grid > d.n_tiles) grid = d.n_tiles;
-  rq_kernel<R><<<(unsigned)grid, threads, smem, s>>>(m, d);
+  e = launch_pdl(rq_kernel<R>, dim3((unsigned)grid), dim3(threads), smem, s, m, d);
   if (launches) ++*launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace
@@ -522,6 +560,12 @@ cudaError_t launch_reorder_quantize(const RqArgs& a, cudaStream_t s, int64_t* la
   if (2 * row_bytes * 3 <= 200 * 1024) return launch_rq_t<2>(a, s, launches);
   return launch_rq_t<1>(a, s, launches);
 }
+
+}  // namespace mmx
+extern "C" int mm_debug_rq_trace(unsigned long long* h, int n) {
+  return (int)cudaMemcpyFromSymbol(h, mmx::g_rq_trace, sizeof(unsigned long long) * (size_t)(n < 2560 ? n : 2560));
+}
+namespace mmx {
 
 cudaError_t launch_reorder_bf16(const uint16_t* x, int64_t rows, int64_t ldx, int K,
                                 const int32_t* perm, uint16_t* xr, int64_t ldxr,

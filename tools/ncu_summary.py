@@ -1,0 +1,104 @@
+"""Summarise an ncu run of tools/profile.sh into profiles/ (tracked):
+
+  profiles/<tag>_launches.csv   kernel, launches, mean/total device time, share of the step
+  profiles/<tag>_kernels.md     per hot kernel: duration, DRAM bytes, L2/tensor/issue utilisation
+  profiles/traffic_<tag>.json   dram bytes per launch (read + write) for bench.py's roofline.traffic
+
+usage: python tools/ncu_summary.py gpurun_out/prof_r01 r01
+"""
+import csv
+import json
+import os
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+RAW_METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % of peak"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (elapsed)"),
+    ("sm__ops_path_tensor_op_utcomma_src_fp4_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+     "MXF4 (UTCOMMA) ops % of peak"),
+    ("sm__ops_path_tensor_op_utcqmma_src_fp4_fp6_fp8_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+     "MXF8F6F4 (UTCQMMA) ops % of peak"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum", "L2->L1/smem read bytes"),
+]
+
+
+def read_raw(path):
+    rows = list(csv.reader(open(path)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    return {h: (v, u) for h, v, u in zip(hdr, vals, units)}
+
+
+def to_bytes(v, u):
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+    return float(v) * scale
+
+
+def main(src, tag):
+    out = os.path.join(ROOT, "profiles")
+    os.makedirs(out, exist_ok=True)
+    # ---- launch list ------------------------------------------------------------------
+    lpath = os.path.join(src, "launches.csv")
+    agg = defaultdict(lambda: [0, 0.0])
+    if os.path.exists(lpath):
+        lines = [l for l in open(lpath) if l.startswith('"')]
+        rdr = csv.reader(lines)
+        hdr = next(rdr)
+        i_name, i_metric, i_val = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+        for r in rdr:
+            if r[i_metric] != "gpu__time_duration.sum":
+                continue
+            name = r[i_name].split("(")[0].replace("void ", "").split("::")[-1]
+            agg[name][0] += 1
+            agg[name][1] += float(r[i_val].replace(",", ""))
+        hot = {k: v for k, v in agg.items() if "rq_kernel" in k or "mixgemm" in k}
+        step_ns = sum(v[1] for v in hot.values())
+        with open(os.path.join(out, f"{tag}_launches.csv"), "w") as f:
+            f.write("kernel,launches,total_ns,mean_ns,share_of_hot_path\n")
+            for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+                share = (t / step_ns) if k in hot and step_ns else 0.0
+                f.write(f"{k},{n},{t:.0f},{t / n:.0f},{share:.3f}\n")
+    # ---- full captures -------------------------------------------------------------------
+    traffic = {}
+    md = [f"# ncu summary {tag}", "",
+          "Source: `ncu --set full --clock-control none` (one launch after warm-up, cold-cache replay;",
+          "serialised, so compare shares with the bench, not absolute times). Produced by",
+          "`tools/profile.sh` + `tools/ncu_summary.py`.", ""]
+    for key, label in (("mixgemm", "mixed GEMM"), ("rq_kernel", "reorder-quantize")):
+        path = os.path.join(src, f"full_{key}_raw.csv")
+        if not os.path.exists(path):
+            continue
+        raw = read_raw(path)
+        kname = raw.get("Kernel Name", ("?", ""))[0]
+        md += [f"## {label}: `{kname[:90]}`", "", "| metric | value |", "|---|---|"]
+        for m, lab in RAW_METRICS:
+            if m in raw:
+                v, u = raw[m]
+                md.append(f"| {lab} (`{m}`) | {v} {u} |")
+        rd = to_bytes(*raw["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in raw else None
+        wr = to_bytes(*raw["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in raw else None
+        if rd is not None and wr is not None:
+            traffic["mixgemm" if key == "mixgemm" else "rq"] = rd + wr
+            md.append(f"| DRAM traffic per launch (read + write) | {rd + wr:.4g} B |")
+        md.append("")
+    with open(os.path.join(out, f"{tag}_kernels.md"), "w") as f:
+        f.write("\n".join(md) + "\n")
+    with open(os.path.join(out, f"traffic_{tag}.json"), "w") as f:
+        json.dump(traffic, f, indent=1)
+    print("\n".join(md))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2])
