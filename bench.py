@@ -173,11 +173,11 @@ def oracle_cpu_rate(M, K, N, budget_s=15.0, seed_layer=0):
     w_bits = bf16_bits(gen_weight(N, K, 3000 + seed_layer))
     wc, wsf, _ = omx.reorder_quantize(w_bits, perm, n)
     Wd = omx.dequantize_segments(wc, wsf)
-    # calibrate the sample size with a small probe, then run ~budget_s of work
-    rows = 8
+    # run row batches of the workload (cycling over the M rows) for ~budget_s of CPU time
+    rows = 64
     total_rows, t_total = 0, 0.0
     while t_total < budget_s:
-        x_bits = bf16_bits(gen_act(rows, K, 1000 + seed_layer, 5000 + total_rows))
+        x_bits = bf16_bits(gen_act(rows, K, 1000 + seed_layer, 5000 + (total_rows % M)))
         t0 = time.perf_counter()
         ac, asf, _ = omx.reorder_quantize(x_bits, perm, n)
         y = omx.dequantize_segments(ac, asf) @ Wd.T
@@ -185,12 +185,10 @@ def oracle_cpu_rate(M, K, N, budget_s=15.0, seed_layer=0):
         dt = time.perf_counter() - t0
         total_rows += rows
         t_total += dt
-        if total_rows >= M:
-            break
-        rows = max(8, min(M - total_rows, int(rows * max(1.0, min(4.0, (budget_s - t_total) / max(dt, 1e-3) / 2)))))
+        rows = max(64, min(M, int(rows * max(1.0, min(4.0, (budget_s - t_total) / max(dt, 1e-3) / 2)))))
     tflops = 2.0 * total_rows * N * K / t_total / 1e12
-    sample = (f"{total_rows} of {M} activation rows (reorder-quantize + fp64 GEMM vs all {N} channels), "
-              f"{t_total:.1f} s; weights quantized offline (untimed)")
+    sample = (f"{total_rows} activation rows ({total_rows / M:.2f} x the M={M} batch; reorder-quantize + fp64 "
+              f"GEMM vs all {N} channels) in {t_total:.1f} s; weights quantized offline (untimed)")
     return tflops, sample, threads, total_rows / t_total
 
 
@@ -314,17 +312,25 @@ def run_gpu(args, rank, world, local):
         torch.cuda.synchronize()
         barrier(world)
         launches = mm.launch_count() - l0
-        # per-kernel pass (same K steps, same rotation): events around each launch give
-        # each kernel's own device duration for the roofline lines
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-        torch.cuda._sleep(int(min(400.0, 1.0 + 0.3 * args.steps) * 1e-3 * 1.9e9))
-        for i in range(args.steps):
-            step(i, evs[i])
-        torch.cuda.synchronize()
+        # per-kernel passes: K back-to-back launches of ONE kernel over the same
+        # rotation, bracketed by two events -> that kernel's average launch duration
+        def kernel_pass(fn):
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(int(min(400.0, 1.0 + 0.2 * args.steps) * 1e-3 * 1.9e9))
+            k0.record(stream)
+            for i in range(args.steps):
+                fn(sets[i % n_sets])
+            k1.record(stream)
+            torch.cuda.synchronize()
+            return k0.elapsed_time(k1) / args.steps
+        rq_ms = kernel_pass(lambda st: mm.mm_reorder_quantize_act(st["x"], plan, out=st["a"], stream=stream))
+        if nshard:
+            gemm_ms = kernel_pass(lambda st: mm.mm_mixed_gemm_bf16_nshard_allgather(
+                st["a"], st["wq"], plan, N, comm, out=st["y"], stage=stage, stream=stream))
+        else:
+            gemm_ms = kernel_pass(lambda st: mm.mm_mixed_gemm_bf16(st["a"], st["wq"], plan, out=st["y"], stream=stream))
         clocks = sampler.stop()
     total_ms = max_over_ranks(t0.elapsed_time(t1), world)
-    rq_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-    gemm_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
     ms = total_ms / args.steps
     flops_rank = 2.0 * M * Ns * K
     units = flops_rank * world * args.steps                       # all ranks' useful FLOPs
@@ -382,8 +388,8 @@ def run_gpu(args, rank, world, local):
                          f"{l2 / 1e6:.0f} MB",
                    "timing": "CUDA events on the launching stream; steps pre-queued behind a device sleep "
                              "(device time; host enqueue cost is in e2e); value/ms_per_step from boundary events "
-                             "only, per-kernel durations (breakdown, roofline) from a second K-step pass with "
-                             "events around every launch"},
+                             "only; per-kernel durations (breakdown, roofline) = K back-to-back launches of that "
+                             "kernel alone over the same rotation / K"},
         "breakdown": {"rq_us": rq_ms * 1e3, "gemm_us": gemm_ms * 1e3,
                       "rq_gbs": rq_gbs, "rq_frac_hbm": rq_gbs / pk["hbm_gbs"],
                       "gemm_tflops": gemm_tflops, "gemm_mix_peak_tflops": pmix,
@@ -422,7 +428,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="micromix", choices=["micromix", "reference"])
     ap.add_argument("--config", default="q_proj", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gemm-bn", type=int, default=0, help="GEMM tile N override (tuning)")
     ap.add_argument("--gemm-stages", type=int, default=0, help="GEMM pipeline stages override (tuning)")
