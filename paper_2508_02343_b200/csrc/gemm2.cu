@@ -61,6 +61,18 @@ struct Gemm2Dev {
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
 };
 
+// Tile raster: groups of up to 8 pair-row blocks (2048 rows of A) sweep all of N
+// before moving on, so a wave of tiles reuses the same A rows from L2 (for large M
+// the whole A does not fit in L2, W of one layer does).
+__device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& mb2, int& nb) {
+  const int G = num_m2 < 8 ? num_m2 : 8;
+  const int per_group = G * num_n;
+  const int grp = t / per_group, r = t - grp * per_group;
+  const int rows = min(G, num_m2 - grp * G);
+  mb2 = grp * G + r % rows;
+  nb = r / rows;
+}
+
 template <int G>
 __device__ __forceinline__ void seg_stage(const Gemm2Dev& p, int j, int& kcoord, int& nmma, int& atoms, int& atom0) {
   const int n = G == 0 ? p.n0 : (G == 1 ? p.n1 : p.n2);
@@ -144,7 +156,8 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       uint32_t phase = 0;
       const uint32_t full0 = ptx::smem_u32(&full[0]);
       for (int t = pair; t < num_tiles; t += npairs) {
-        const int mb2 = t % num_m2, nb = t / num_m2;
+        int mb2, nb;
+        tile_coords(t, num_m2, p.num_n, mb2, nb);
         const int m0 = mb2 * 256 + 128 * (int)rank;      // this CTA's A rows
         const int n0 = nb * 256 + 128 * (int)rank;       // this CTA's W rows (its half of N)
         const int mgrp = mb2 * 2 + (int)rank;           // 128-row scale group of A
@@ -283,7 +296,8 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     uint8_t* stg = sEpi + q * 2 * 2048;
     int it = 0, nstore = 0;
     for (int t = pair; t < num_tiles; t += npairs, ++it) {
-      const int mb2 = t % num_m2, nb = t / num_m2;
+      int mb2, nb;
+      tile_coords(t, num_m2, p.num_n, mb2, nb);
       const int acc = it & 1;
       ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), (it >> 1) & 1, 24, it, t);
       if (trace && q == 0 && it < 3) g_trace[blockIdx.x][9 + it] = ptx::globaltimer_ns();
