@@ -52,6 +52,7 @@ def main(src, tag):
     # ---- launch list ------------------------------------------------------------------
     lpath = os.path.join(src, "launches.csv")
     agg = defaultdict(lambda: [0, 0.0])
+    seq = []   # (kernel, ns) in launch order
     if os.path.exists(lpath):
         lines = [l for l in open(lpath) if l.startswith('"')]
         rdr = csv.reader(lines)
@@ -61,15 +62,24 @@ def main(src, tag):
             if r[i_metric] != "gpu__time_duration.sum":
                 continue
             name = r[i_name].split("(")[0].replace("void ", "").split("::")[-1]
+            ns = float(r[i_val].replace(",", ""))
             agg[name][0] += 1
-            agg[name][1] += float(r[i_val].replace(",", ""))
-        hot = {k: v for k, v in agg.items() if "rq_kernel" in k or "mixgemm" in k}
-        step_ns = sum(v[1] for v in hot.values())
+            agg[name][1] += ns
+            seq.append((name, ns))
+        # step shares: every step launches one RQ then one GEMM; the RQ launches before
+        # the first GEMM are the offline weight quantizations and are excluded
+        first_gemm = next((i for i, (k, _) in enumerate(seq) if "mixgemm" in k), len(seq))
+        step_rq = [ns for i, (k, ns) in enumerate(seq) if "rq_kernel" in k and i >= first_gemm - 1]
+        step_gemm = [ns for k, ns in seq if "mixgemm" in k]
+        mean_rq = sum(step_rq) / max(len(step_rq), 1)
+        mean_gemm = sum(step_gemm) / max(len(step_gemm), 1)
         with open(os.path.join(out, f"{tag}_launches.csv"), "w") as f:
-            f.write("kernel,launches,total_ns,mean_ns,share_of_hot_path\n")
+            f.write("kernel,launches,total_ns,mean_ns\n")
             for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-                share = (t / step_ns) if k in hot and step_ns else 0.0
-                f.write(f"{k},{n},{t:.0f},{t / n:.0f},{share:.3f}\n")
+                f.write(f"{k},{n},{t:.0f},{t / n:.0f}\n")
+            f.write(f"# step launches only: rq mean {mean_rq:.0f} ns over {len(step_rq)}, gemm mean "
+                    f"{mean_gemm:.0f} ns over {len(step_gemm)}; gemm share of the step "
+                    f"{mean_gemm / max(mean_rq + mean_gemm, 1):.3f}\n")
     # ---- full captures -------------------------------------------------------------------
     traffic = {}
     md = [f"# ncu summary {tag}", "",
