@@ -22,6 +22,9 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -58,6 +61,9 @@ struct Gemm2Dev {
   uint32_t idesc0, idesc1, idesc2;
   uint16_t* y;
   int64_t ldy;
+  int stream_k;                   // 1: stream-K split of the K loop over pairs (see work_item)
+  float* ws;                      // stream-K partial tiles: [npairs][256 rows][256 cols] fp32
+  int* ws_flag;                   // per pair: 8 epilogue warps arrive (+1), the finisher consumes (-1)
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
 };
 
@@ -71,6 +77,31 @@ __device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& m
   const int rows = min(G, num_m2 - grp * G);
   mb2 = grp * G + r % rows;
   nb = r / rows;
+}
+
+// Work items of pair `pair`.  Data-parallel: whole tiles pair, pair + npairs, ...
+// Stream-K (opt-in, when the tile count leaves a ragged last wave): the T x S stage
+// iterations (S = stages per tile) are cut into npairs contiguous ranges; a range
+// covers the tail of one tile (this pair finishes it: adds the partial the
+// previous pair left in the workspace), whole tiles, and the head of another
+// (this pair leaves a partial for the next pair).  Items run in DESCENDING tile
+// order, so every pair writes its partial head first and the finisher of that
+// tile -- the next pair, at the end of its own range -- finds it ready.
+__device__ __forceinline__ int num_items(const Gemm2Dev& p, int pair, int npairs, int S) {
+  if (!p.stream_k) return (p.num_tiles - pair + npairs - 1) / npairs;
+  const int64_t W = (int64_t)p.num_tiles * S;
+  const int64_t lo = pair * W / npairs, hi = (pair + 1) * W / npairs;
+  return hi > lo ? (int)((hi - 1) / S - lo / S + 1) : 0;
+}
+__device__ __forceinline__ void work_item(const Gemm2Dev& p, int pair, int npairs, int S, int i, int& t, int& s0,
+                                          int& s1) {
+  if (!p.stream_k) { t = pair + i * npairs; s0 = 0; s1 = S; return; }
+  const int64_t W = (int64_t)p.num_tiles * S;
+  const int64_t lo = pair * W / npairs, hi = (pair + 1) * W / npairs;
+  t = (int)((hi - 1) / S) - i;
+  const int64_t base = (int64_t)t * S;
+  s0 = (int)(lo > base ? lo - base : 0);
+  s1 = (int)(hi - base < S ? hi - base : S);
 }
 
 template <int G>
@@ -147,7 +178,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   ptx::grid_dep_wait();   // A, W, scales may come from the preceding kernel; Y may still be read by it
   if (trace && warp == 1) { g_trace[blockIdx.x][0] = t_start; g_trace[blockIdx.x][1] = ptx::globaltimer_ns(); }
   const int64_t M = p.M, N = p.N;
-  const int num_m2 = p.num_m2, num_tiles = p.num_tiles;
+  const int num_m2 = p.num_m2;
+  const int S = p.nst0 + p.nst1 + p.nst2;
+  const int n_items = num_items(p, pair, npairs, S);
 
   if (warp == 0) {
     // ============================ TMA producer (both CTAs) ============================
@@ -155,7 +188,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t full0 = ptx::smem_u32(&full[0]);
-      for (int t = pair; t < num_tiles; t += npairs) {
+      for (int it = 0; it < n_items; ++it) {
+        int t, s0, s1;
+        work_item(p, pair, npairs, S, it, t, s0, s1);
         int mb2, nb;
         tile_coords(t, num_m2, p.num_n, mb2, nb);
         const int m0 = mb2 * 256 + 128 * (int)rank;      // this CTA's A rows
@@ -174,7 +209,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
           // as 128 B per smem row but completes 96 B per row.
           const uint32_t ab = g == 1 ? (A_BYTES + B_BYTES) / 4 * 3 : (A_BYTES + B_BYTES);
           const uint32_t cta_bytes = ab + 3u * box_atoms * 512u;
-          for (int j = 0; j < nst; ++j) {
+          const int sbase = g == 0 ? 0 : (g == 1 ? p.nst0 : p.nst0 + p.nst1);
+          const int j_lo = max(s0 - sbase, 0), j_hi = min(s1 - sbase, nst);
+          for (int j = j_lo; j < j_hi; ++j) {
             int kcoord, nmma, atoms, atom0;
             if (g == 0) seg_stage<0>(p, j, kcoord, nmma, atoms, atom0);
             else if (g == 1) seg_stage<1>(p, j, kcoord, nmma, atoms, atom0);
@@ -216,7 +253,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       const uint32_t sSFA0 = ptx::smem_u32(sSFA), sSFB0 = ptx::smem_u32(sSFB);
       const uint32_t empty0 = ptx::smem_u32(&empty[0]), full0 = ptx::smem_u32(&full[0]);
       const bool no_mma = (p.dbg & 2) != 0;
-      for (int t = pair; t < num_tiles; t += npairs, ++it) {
+      for (; it < n_items; ++it) {
+        int t, s0, s1;
+        work_item(p, pair, npairs, S, it, t, s0, s1);
         const int acc = it & 1;
         const uint32_t d_t = tmem_base + (acc ? ACC1_COL : 0);
         ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), ((it >> 1) & 1) ^ 1, 22, it, t);   // tile it-2 drained acc
@@ -232,10 +271,12 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
           const uint32_t idesc = g == 0 ? p.idesc0 : (g == 1 ? p.idesc1 : p.idesc2);
           const int kstage = g == 0 ? 256 : 128;                    // K per stage
           const int kmma = g == 0 ? 64 : 32;                        // K per MMA
-          for (int j = 0; j < nst; ++j) {
+          const int sbase = g == 0 ? 0 : (g == 1 ? p.nst0 : p.nst0 + p.nst1);
+          const int j_lo = max(s0 - sbase, 0), j_hi = min(s1 - sbase, nst);
+          for (int j = j_lo; j < j_hi; ++j) {
             const int nmma = min((n_g - kstage * j + kmma - 1) / kmma, 4);
             ptx::mbar_wait(full0 + 8 * stage, phase, 23, stage, t);
-            if (trace && it == 0 && g == 0 && j == 0) g_trace[blockIdx.x][2] = ptx::globaltimer_ns();
+            if (trace && it == 0 && j == j_lo && g == 0) g_trace[blockIdx.x][2] = ptx::globaltimer_ns();
             ptx::tc_fence_after();
             const uint32_t sfa_t = tmem_base + SF_COL + (stage & 1) * SF_STRIDE;
             const uint32_t sfb_t = sfa_t + 8;
@@ -294,10 +335,23 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
     const uint32_t tovl_leader = ptx::mapa(ptx::smem_u32(&tovl[0]), 0);
     uint8_t* stg = sEpi + q * 2 * 2048;
-    int it = 0, nstore = 0;
-    for (int t = pair; t < num_tiles; t += npairs, ++it) {
+    int nstore = 0;
+    for (int it = 0; it < n_items; ++it) {
+      int t, s0, s1;
+      work_item(p, pair, npairs, S, it, t, s0, s1);
       int mb2, nb;
       tile_coords(t, num_m2, p.num_n, mb2, nb);
+      // stream-K roles of this item: leave a partial (head of a tile) / add one (tail)
+      const bool to_ws = s1 < S, from_ws = s0 > 0;
+      const int wrow = 128 * (int)rank + q * 32 + lane;   // row inside the 256-row pair tile
+      if (from_ws) {   // wait until the previous pair's 8 epilogue warps published its partial
+        if (lane == 0) {
+          volatile int* f = p.ws_flag + (pair - 1);
+          while (*f < 8) __nanosleep(64);
+        }
+        __syncwarp();
+        __threadfence();
+      }
       const int acc = it & 1;
       ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), (it >> 1) & 1, 24, it, t);
       if (trace && q == 0 && it < 3) g_trace[blockIdx.x][9 + it] = ptx::globaltimer_ns();
@@ -319,6 +373,25 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
           if (lane == 0) ptx::mbar_arrive_cluster((i == 1 ? tovl_leader : tempty_leader) + 8 * acc);
         }
         if (p.dbg & 4) continue;
+        if (to_ws) {   // fp32 partial -> workspace row (128 B per chunk per thread)
+          float4* dst = reinterpret_cast<float4*>(p.ws + ((size_t)pair * 256 + wrow) * 256 + 32 * c);
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                 __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+          continue;
+        }
+        if (from_ws) {   // add the previous pair's partial (fixed order: partial + own)
+          const float4* src = reinterpret_cast<const float4*>(p.ws + ((size_t)(pair - 1) * 256 + wrow) * 256 + 32 * c);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const float4 o = __ldcg(src + v);
+            r[4 * v] = __float_as_uint(o.x + __uint_as_float(r[4 * v]));
+            r[4 * v + 1] = __float_as_uint(o.y + __uint_as_float(r[4 * v + 1]));
+            r[4 * v + 2] = __float_as_uint(o.z + __uint_as_float(r[4 * v + 2]));
+            r[4 * v + 3] = __float_as_uint(o.w + __uint_as_float(r[4 * v + 3]));
+          }
+        }
         uint32_t w[16];
 #pragma unroll
         for (int v = 0; v < 16; ++v) w[v] = ptx::pack_bf16x2(__uint_as_float(r[2 * v]), __uint_as_float(r[2 * v + 1]));
@@ -338,6 +411,15 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
           ptx::bulk_commit_group();
         }
         ++nstore;
+      }
+      if (to_ws) {   // publish: this warp's rows of the partial are in global memory
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.ws_flag + pair, 1);
+      }
+      if (from_ws) {  // consumed: hand the slot back (8 x -1 returns it to 0)
+        __syncwarp();
+        if (lane == 0) atomicSub(p.ws_flag + (pair - 1), 1);
       }
     }
     if (lane == 0) ptx::bulk_wait_group_read<0>();
@@ -363,6 +445,34 @@ bool make_sf_map(CUtensorMap* m, const void* base, int64_t rows, int kp, int box
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Library-owned stream-K workspace, one per (device, stream), allocated on first
+// use and grown as needed: [npairs][256][256] fp32 partial tiles + npairs flags
+// (zeroed once; the kernel leaves them at zero).  Not touched by data-parallel runs.
+bool stream_k_workspace(cudaStream_t s, int npairs, float** ws, int** flags) {
+  static std::mutex mu;
+  struct Ent { float* ws = nullptr; int* flags = nullptr; int npairs = 0; };
+  static std::map<std::pair<int, cudaStream_t>, Ent> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  Ent& e = cache[{dev, s}];
+  if (e.npairs < npairs) {
+    if (e.ws) cudaFree(e.ws);
+    if (e.flags) cudaFree(e.flags);
+    e.ws = nullptr;
+    e.flags = nullptr;
+    e.npairs = 0;
+    if (cudaMalloc(&e.ws, (size_t)npairs * 256 * 256 * sizeof(float)) != cudaSuccess) return false;
+    if (cudaMalloc(&e.flags, (size_t)npairs * sizeof(int)) != cudaSuccess) return false;
+    if (cudaMemset(e.flags, 0, (size_t)npairs * sizeof(int)) != cudaSuccess) return false;
+    if (cudaDeviceSynchronize() != cudaSuccess) return false;
+    e.npairs = npairs;
+  }
+  *ws = e.ws;
+  *flags = e.flags;
+  return true;
 }
 
 template <int STAGES>
@@ -416,13 +526,28 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.ldy = a.ldy;
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   if (p.num_tiles == 0) return cudaSuccess;
+  int grid = sm_count() & ~1;
+  if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas & ~1;
+  if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
+  // Stream-K when the last wave of tiles would be ragged and there are only a few
+  // waves (each pair then finishes at most one tile left by its neighbour).
+  const int npairs = grid / 2;
+  // Opt-in (MM_GEMM_STREAMK=1): measured on q_proj it LOSES (40.9 vs 29.6 us) -- each
+  // extra work item costs a full TMEM drain plus a 256 KB fp32 partial round trip,
+  // more than the ragged wave it removes.  Kept as a tested alternative schedule.
+  const bool sk_env_on = [] { const char* e = getenv("MM_GEMM_STREAMK"); return e && atoi(e) == 1; }();
+  p.stream_k = (sk_env_on && !cfg.no_stream_k && p.num_tiles > npairs && p.num_tiles % npairs != 0 &&
+                p.num_tiles < 4 * npairs) ? 1 : 0;
+  if (p.stream_k) {
+    if (!stream_k_workspace(s, npairs, &p.ws, &p.ws_flag)) {
+      *err = "stream-K workspace allocation failed";
+      return cudaErrorMemoryAllocation;
+    }
+  }
   const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + EPI_BYTES + (2 * STAGES + 6) * 8 + 16;
   auto kern = mixgemm2_kernel<STAGES>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
-  int grid = sm_count() & ~1;
-  if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas & ~1;
-  if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
   e = launch_pdl(kern, dim3(grid), dim3(kThreads2), smem, s, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
                  maps[6], maps[7], maps[8], maps[9], maps[10], maps[11], maps[12], p);
   if (launches) ++*launches;

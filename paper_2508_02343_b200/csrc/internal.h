@@ -61,6 +61,7 @@ struct GemmConfig {
   int block_n = 0;      // 0 = auto
   int num_stages = 0;   // 0 = auto
   int max_ctas = 0;     // 0 = #SMs
+  bool no_stream_k = false;  // keep the data-parallel tiling (N-shard path: shard-independent results)
 };
 
 // Mixed block-scaled GEMM (gemm.cu).

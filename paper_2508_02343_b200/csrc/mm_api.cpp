@@ -389,7 +389,7 @@ mm_status mm_reorder_act_bf16(const void* d_x, int64_t M, int64_t ldx, const mm_
 }
 
 static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const mm_plan* plan, void* d_y,
-                             int64_t ldy, int64_t n_cols, mm_stream_t stream) {
+                             int64_t ldy, int64_t n_cols, mm_stream_t stream, bool no_stream_k = false) {
   mm_status st = check_device();
   if (st != MM_OK) return st;
   if ((st = validate_plan(plan)) != MM_OK) return st;
@@ -421,6 +421,7 @@ static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const
     std::lock_guard<std::mutex> lk(g_cfg_mu);
     cfg = g_gemm_cfg;
   }
+  cfg.no_stream_k = cfg.no_stream_k || no_stream_k;
   const char* err = "";
   cudaError_t e = launch_mixed_gemm(ga, cfg, reinterpret_cast<cudaStream_t>(stream), &g_launches, &err);
   if (e != cudaSuccess) return fail(MM_ERR_CUDA, "mixed GEMM launch: %s (%s)", cudaGetErrorString(e), err);
@@ -490,7 +491,7 @@ mm_status mm_mixed_gemm_bf16_nshard_allgather(const mm_mx_tensor* a, const mm_mx
   const int64_t M = a->rows;
   uint16_t* stage = static_cast<uint16_t*>(d_stage);
   uint16_t* mine = stage + (int64_t)c->rank * M * Ns;
-  mm_status st = gemm_common(a, w_shard, plan, mine, Ns, Ns, stream);
+  mm_status st = gemm_common(a, w_shard, plan, mine, Ns, Ns, stream, /*no_stream_k=*/true);
   if (st != MM_OK) return st;
   if (M == 0 || Ns == 0) return MM_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -178,3 +178,26 @@ def test_llama70b_down_sampled():
     yref, ybf = _ref(xs, ws, plan)
     ys = y[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()]
     _check(ys, yref, ybf)
+
+
+@pytest.mark.parametrize("M,N,n", [(2500, 2048, (2240, 1184, 672)), (2048, 4096, (1024, 1024, 2048))])
+def test_stream_k_matches_oracle_and_data_parallel(M, N, n, monkeypatch):
+    """Tile counts just above the number of CTA pairs with MM_GEMM_STREAMK=1 take the
+    stream-K schedule (partial tiles through the workspace).  Checked against the
+    oracle at the 2e-3 bar, and against the data-parallel schedule (only the FP32
+    summation order of split tiles differs)."""
+    K = sum(n)
+    x = gen_act(M, K, 1003, 2600)
+    w = gen_weight(N, K, 3600)
+    plan = mm.mm_plan_init(K, n, gen_perm(K, 14))
+    monkeypatch.setenv("MM_GEMM_STREAMK", "1")
+    y_sk = _run(x, w, plan)
+    monkeypatch.setenv("MM_GEMM_STREAMK", "0")
+    y_dp = _run(x, w, plan)
+    rows = np.arange(0, M, 7)
+    yref, ybf = _ref(x, w, plan, rows=rows)
+    _check(y_sk[torch.from_numpy(rows).cuda()], yref, ybf)
+    _check(y_dp[torch.from_numpy(rows).cuda()], yref, ybf)
+    a, b = y_sk.double().cpu().numpy(), y_dp.double().cpu().numpy()
+    assert ogemm.rel_fro(a, b) < 1e-3
+    assert not np.array_equal(a, b) or True   # identical is fine too (no split tile)
