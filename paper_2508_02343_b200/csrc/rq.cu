@@ -273,7 +273,7 @@ struct RqDev {
 //    16-byte vectors), block amax, scale and encode as above; finally the stage
 //    is released to the producer.
 template <int R>
-__global__ void __launch_bounds__(704, 1)
+__global__ void __launch_bounds__(R == 4 ? 704 : 1024, 1)
 rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev d) {
   using ST = typename Slot<R>::T;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -508,7 +508,7 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   if (gw > 12) gw = 12;
   if (gw < 2) gw = 2;
   d.group_warps = gw;
-  int groups = 21 / gw;   // <= 21 consumer warps + the producer warp (register budget)
+  int groups = (R == 4 ? 21 : 31) / gw;   // consumer warps (+ the producer warp) within the register budget
   if (groups > stages - 1) groups = stages - 1;
   if (groups < 1) groups = 1;
   d.groups = groups;
@@ -554,9 +554,14 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
 
 cudaError_t launch_reorder_quantize(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   if (a.rows == 0) return cudaSuccess;
-  // Rows per tile: 4 while a stage of 4 rows leaves room for >= 4 stages, then 2, 1.
   const size_t row_bytes = (size_t)((a.K + 255) / 256) * 512;
-  if (4 * row_bytes * 4 <= 200 * 1024) return launch_rq_t<4>(a, s, launches);
+  static const int force_r = [] { const char* e = getenv("MM_RQ_ROWS"); return e ? atoi(e) : 0; }();  // tuning
+  if (force_r == 2) return launch_rq_t<2>(a, s, launches);
+  if (force_r == 1) return launch_rq_t<1>(a, s, launches);
+  if (force_r == 4) return launch_rq_t<4>(a, s, launches);
+  // Two-row tiles while >= 3 stages fit (measured faster than four-row tiles at
+  // q_proj: twice the tiles balance the persistent grid, fewer registers per lane
+  // allow more consumer warps), single rows beyond.
   if (2 * row_bytes * 3 <= 200 * 1024) return launch_rq_t<2>(a, s, launches);
   return launch_rq_t<1>(a, s, launches);
 }
