@@ -134,6 +134,36 @@ mm_status mm_calibrate_thresholds(const void* d_x, int64_t L, int32_t K, int64_t
                                   void* d_ws, size_t ws_bytes,
                                   double* h_chmax, double* h_chmean, mm_stream_t stream);
 
+/* Streaming calibration (the paper pools 32 x 2048 calibration tokens per layer,
+ * §4.1; pooled statistics, R15).  d_state: caller-owned device
+ * buffer of mm_calib_state_bytes(K) bytes, 256-byte aligned, ZEROED before the first
+ * batch.  mm_calib_accumulate adds one batch X[L, K] (exact channel max, double-double
+ * channel |x| sums, row count) -- asynchronous; d_ws as for mm_calibrate_thresholds.
+ * mm_calib_finalize turns the state into a plan exactly as mm_calibrate_thresholds
+ * does over the concatenated batches (SYNCHRONIZES stream); h_rows (may be NULL)
+ * receives the pooled row count.  MM_ERR_DEGENERATE if no rows or max|X| == 0. */
+int64_t mm_calib_state_bytes(int32_t K);
+mm_status mm_calib_accumulate(const void* d_x, int64_t L, int32_t K, int64_t ldx, void* d_ws, size_t ws_bytes,
+                              void* d_state, mm_stream_t stream);
+mm_status mm_calib_finalize(const void* d_state, int32_t K, int32_t fmt6, int32_t fmt8, int32_t rule,
+                            int32_t* d_perm_out, mm_plan* plan_out, double* h_chmax, double* h_chmean,
+                            int64_t* h_rows, mm_stream_t stream);
+
+/* Plan diagnostics (host only): proportions p4/p6/p8 (§3.1 Q2), average bits per
+ * element incl. the 8-bit scale per 32 elements (Table 1 accounting, SPEC.md line
+ * 392), stored bytes per row (128-padded segments + scale bytes), and -- when the
+ * calibration channel maxima h_chmax[K] and the host permutation h_perm[K] are
+ * given -- the Eq. 6 violations: channels placed in P4 (P6) by their mean whose
+ * max exceeds T(4) (T(6)). */
+typedef struct {
+  double p[3];
+  double avg_bits;
+  int64_t stored_bytes_per_row;
+  int32_t eq6_violations[2];
+} mm_plan_diag;
+mm_status mm_plan_diagnostics(const mm_plan* plan, const double* h_chmax, const int32_t* h_perm,
+                              mm_plan_diag* out);
+
 /* Offline weight transform (Fig. 1 caption line 20; line 151): W[N, K] BF16
  * (PyTorch Linear layout, K contiguous, ld = ldw) is reordered with the plan's
  * permutation and block-quantized along K into w_out (rows = N). */

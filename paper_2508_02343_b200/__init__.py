@@ -35,6 +35,7 @@ EXPORTS = [
     "mm_reorder_act_bf16", "mm_set_gemm_config", "mm_launch_count", "mm_reset_launch_count",
     "mm_last_error", "mm_abi_version", "mm_nccl_unique_id_bytes", "mm_nccl_get_unique_id",
     "mm_comm_init", "mm_comm_destroy", "mm_mixed_gemm_bf16_nshard_allgather",
+    "mm_calib_state_bytes", "mm_calib_accumulate", "mm_calib_finalize", "mm_plan_diagnostics",
 ]
 
 
@@ -50,6 +51,11 @@ class CPlan(ctypes.Structure):
                 ("d_perm", ctypes.c_void_p), ("fingerprint", ctypes.c_uint64),
                 ("tensor_max", ctypes.c_double), ("t4", ctypes.c_double), ("t6", ctypes.c_double),
                 ("c", ctypes.c_int32 * 3), ("reserved2", ctypes.c_int32)]
+
+
+class CDiag(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_double * 3), ("avg_bits", ctypes.c_double), ("stored_bytes_per_row", ctypes.c_int64),
+                ("eq6_violations", ctypes.c_int32 * 2)]
 
 
 class CMx(ctypes.Structure):
@@ -97,6 +103,10 @@ def lib(build_if_missing: bool = False):
             "mm_comm_init": (ctypes.c_int, [i32, i32, vp, ctypes.POINTER(vp)]),
             "mm_comm_destroy": (ctypes.c_int, [vp]),
             "mm_mixed_gemm_bf16_nshard_allgather": (ctypes.c_int, [X, X, P, i64, vp, i64, vp, vp, vp]),
+            "mm_calib_state_bytes": (i64, [i32]),
+            "mm_calib_accumulate": (ctypes.c_int, [vp, i64, i32, i64, vp, ctypes.c_size_t, vp, vp]),
+            "mm_calib_finalize": (ctypes.c_int, [vp, i32, i32, i32, i32, vp, P, vp, vp, vp, vp]),
+            "mm_plan_diagnostics": (ctypes.c_int, [P, vp, vp, ctypes.POINTER(CDiag)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -215,6 +225,46 @@ def mm_calibrate_thresholds(x: torch.Tensor, fmt6=MM_E3M2, fmt8=MM_E4M3, rule=MM
                                          _stream()))
     plan = Plan(c, d_perm)
     return (plan, chmax, chmean) if return_stats else plan
+
+
+class CalibState:
+    """Streaming calibration (include/mm.h mm_calib_*): accumulate batches, then finalize."""
+
+    def __init__(self, K: int, device="cuda"):
+        self.K = K
+        self.buf = torch.zeros(lib().mm_calib_state_bytes(K), dtype=torch.uint8, device=device)
+
+    def accumulate(self, x: torch.Tensor):
+        assert x.dtype == torch.bfloat16 and x.dim() == 2 and x.stride(1) == 1 and x.shape[1] == self.K
+        L = x.shape[0]
+        ws = torch.empty(max(lib().mm_calib_workspace_bytes(L, self.K), 1), dtype=torch.uint8, device=x.device)
+        _check(lib().mm_calib_accumulate(_ptr(x), L, self.K, x.stride(0), _ptr(ws), ws.numel(), _ptr(self.buf),
+                                         _stream()))
+        self._ws = ws   # keep alive until the queued work ran
+        return self
+
+    def finalize(self, fmt6=MM_E3M2, fmt8=MM_E4M3, rule=MM_SCALE_OCP, return_stats=False):
+        d_perm = torch.empty(self.K, dtype=torch.int32, device=self.buf.device)
+        chmax = torch.empty(self.K, dtype=torch.float64)
+        chmean = torch.empty(self.K, dtype=torch.float64)
+        rows = ctypes.c_int64(0)
+        c = CPlan()
+        _check(lib().mm_calib_finalize(_ptr(self.buf), self.K, fmt6, fmt8, rule, _ptr(d_perm), ctypes.byref(c),
+                                       ctypes.c_void_p(chmax.data_ptr()), ctypes.c_void_p(chmean.data_ptr()),
+                                       ctypes.byref(rows), _stream()))
+        plan = Plan(c, d_perm)
+        return (plan, chmax, chmean, rows.value) if return_stats else plan
+
+
+def mm_plan_diagnostics(plan: Plan, chmax=None) -> dict:
+    """p4/p6/p8, average bits (Table 1 accounting), stored bytes per row, Eq. 6 violations."""
+    d = CDiag()
+    perm = plan.perm_host().contiguous() if chmax is not None else None
+    cm = torch.as_tensor(chmax, dtype=torch.float64).contiguous() if chmax is not None else None
+    _check(lib().mm_plan_diagnostics(ctypes.byref(plan.c), ctypes.c_void_p(cm.data_ptr()) if cm is not None else None,
+                                     ctypes.c_void_p(perm.data_ptr()) if perm is not None else None, ctypes.byref(d)))
+    return {"p": tuple(d.p), "avg_bits": d.avg_bits, "stored_bytes_per_row": d.stored_bytes_per_row,
+            "eq6_violations": tuple(d.eq6_violations)}
 
 
 def _rq(fn, x: torch.Tensor, plan: Plan, out: MXTensor | None, stream=None) -> MXTensor:

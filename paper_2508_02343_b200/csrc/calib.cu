@@ -9,7 +9,9 @@
 //     division by L -- the correctly rounded fp64 mean in all but
 //     astronomically rare cases (reading R26).
 #include <cuda_runtime.h>
+#include <cmath>
 #include <cstdint>
+#include <cstring>
 
 #include "internal.h"
 
@@ -97,6 +99,23 @@ __global__ void calib_finalize(const Partial* __restrict__ part, int splits, int
   chmean[k] = q1 + r / dl;
 }
 
+// Streaming calibration: add one batch's split partials into the running state
+// (per channel: double-double |x| sum and max |x| bits; header: total rows).
+__global__ void calib_merge(const Partial* __restrict__ part, int splits, int K, int64_t L,
+                            Partial* __restrict__ state, int64_t* __restrict__ rows) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k == 0) *rows += L;
+  if (k >= K) return;
+  DD acc{state[k].hi, state[k].lo};
+  uint32_t m = state[k].mx;
+  for (int s = 0; s < splits; ++s) {
+    Partial p = part[(int64_t)s * K + k];
+    acc = dd_add_dd(acc, DD{p.hi, p.lo});
+    m = max(m, p.mx);
+  }
+  state[k] = {acc.hi, acc.lo, m, 0};
+}
+
 int calib_splits(int64_t L, int K) {
   const int colblocks = (K + kThreadsX * kColsPerThread - 1) / (kThreadsX * kColsPerThread);
   int want = (4 * sm_count() + colblocks - 1) / colblocks;
@@ -126,6 +145,42 @@ cudaError_t launch_calib_stats(const uint16_t* x, int64_t L, int64_t ldx, int K,
                                                  L, d_chmax, d_chmean);
   if (launches) ++*launches;
   return cudaGetLastError();
+}
+
+size_t calib_state_bytes(int K) { return 256 + (size_t)K * sizeof(Partial); }
+
+cudaError_t launch_calib_accumulate(const uint16_t* x, int64_t L, int64_t ldx, int K, void* ws, void* state,
+                                    cudaStream_t s, int64_t* launches) {
+  const int splits = calib_splits(L, K);
+  dim3 grid((K + kThreadsX * kColsPerThread - 1) / (kThreadsX * kColsPerThread), splits);
+  dim3 block(kThreadsX, kRowGroups);
+  calib_pass<<<grid, block, 0, s>>>(x, L, ldx, K, splits, reinterpret_cast<Partial*>(ws));
+  if (launches) ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  uint8_t* st = static_cast<uint8_t*>(state);
+  calib_merge<<<(K + 255) / 256, 256, 0, s>>>(reinterpret_cast<const Partial*>(ws), splits, K, L,
+                                              reinterpret_cast<Partial*>(st + 256), reinterpret_cast<int64_t*>(st));
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+void calib_state_to_stats(const void* h_state, int K, double* chmax, double* chmean, int64_t* rows) {
+  const uint8_t* st = static_cast<const uint8_t*>(h_state);
+  const int64_t L = *reinterpret_cast<const int64_t*>(st);
+  const Partial* p = reinterpret_cast<const Partial*>(st + 256);
+  const double dl = (double)L;
+  for (int k = 0; k < K; ++k) {
+    uint32_t b = p[k].mx << 16;
+    float f;
+    memcpy(&f, &b, 4);
+    chmax[k] = (double)f;
+    // the same compensated division as calib_finalize (fma is exact-rounded on host too)
+    const double q1 = p[k].hi / dl;
+    const double r = std::fma(-q1, dl, p[k].hi) + p[k].lo;
+    chmean[k] = L > 0 ? q1 + r / dl : 0.0;
+  }
+  *rows = L;
 }
 
 }  // namespace mmx

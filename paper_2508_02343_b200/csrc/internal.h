@@ -46,6 +46,13 @@ cudaError_t launch_calib_stats(const uint16_t* x, int64_t L, int64_t ldx, int K,
                                void* ws, double* d_chmax, double* d_chmean,
                                cudaStream_t s, int64_t* launches);
 
+// Streaming calibration (calib.cu): state = [256-byte header: int64 rows][K x 24-byte
+// per-channel partials]; accumulate adds one batch; the host turns the state into stats.
+size_t calib_state_bytes(int K);
+cudaError_t launch_calib_accumulate(const uint16_t* x, int64_t L, int64_t ldx, int K, void* ws, void* state,
+                                    cudaStream_t s, int64_t* launches);
+void calib_state_to_stats(const void* h_state, int K, double* chmax, double* chmean, int64_t* rows);
+
 struct GemmArgs {
   int64_t M, N;
   SegGeom geom;

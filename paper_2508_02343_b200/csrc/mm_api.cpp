@@ -303,6 +303,43 @@ mm_status mm_plan_init(mm_plan* out, int32_t K, const int32_t n[3], int32_t fmt6
   return MM_OK;
 }
 
+// Host half of calibration, shared by the one-shot and the streaming paths.
+static mm_status plan_from_stats(const std::vector<double>& chmax, const std::vector<double>& chmean, int32_t K,
+                                 int32_t fmt6, int32_t fmt8, int32_t rule, int32_t* d_perm_out, mm_plan* plan_out,
+                                 mm_stream_t stream) {
+  // Eq. 5: T(n) = 2^(b+n-1) max|X| / (254 q_max), one correctly rounded division.
+  double tmax = 0.0;
+  for (double v : chmax) tmax = std::max(tmax, v);
+  if (!(tmax > 0.0)) return fail(MM_ERR_DEGENERATE, "calibration data has max|X| == 0");
+  const double t4 = (std::ldexp(1.0, bias_of(F_E2M1) + 4 - 1) * tmax) / (254.0 * qmax_of(F_E2M1));
+  const double t6 = (std::ldexp(1.0, bias_of(fmt6) + 6 - 1) * tmax) / (254.0 * qmax_of(fmt6));
+  // Eq. 6 / Eq. 17: channel counts by channel max.
+  int32_t c4 = 0, c6 = 0;
+  for (double v : chmax) {
+    if (v <= t4) ++c4;
+    else if (v <= t6) ++c6;
+  }
+  const int32_t c8 = K - c4 - c6;
+  // Rounding to whole 32-blocks: n8 up, then n6 up (capped), n4 the remainder.
+  int32_t n[3];
+  n[2] = (int32_t)roundup(c8, 32);
+  n[1] = std::min((int32_t)roundup(c6, 32), K - n[2]);
+  n[0] = K - n[2] - n[1];
+  // Eq. 7 + Q3: stable ascending argsort of the channel means.
+  std::vector<int32_t> perm(K);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return chmean[a] < chmean[b]; });
+  mm_status st = mm_plan_init(plan_out, K, n, fmt6, fmt8, rule, perm.data(), d_perm_out, stream);
+  if (st != MM_OK) return st;
+  plan_out->tensor_max = tmax;
+  plan_out->t4 = t4;
+  plan_out->t6 = t6;
+  plan_out->c[0] = c4;
+  plan_out->c[1] = c6;
+  plan_out->c[2] = c8;
+  return MM_OK;
+}
+
 mm_status mm_calibrate_thresholds(const void* d_x, int64_t L, int32_t K, int64_t ldx, int32_t fmt6, int32_t fmt8,
                                   int32_t rule, int32_t* d_perm_out, mm_plan* plan_out, void* d_ws, size_t ws_bytes,
                                   double* h_chmax, double* h_chmean, mm_stream_t stream) {
@@ -330,37 +367,76 @@ mm_status mm_calibrate_thresholds(const void* d_x, int64_t L, int32_t K, int64_t
   if (e == cudaSuccess) e = cudaMemcpyAsync(chmean.data(), d_chmean, (size_t)K * 8, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "calibration statistics");
-  // Eq. 5: T(n) = 2^(b+n-1) max|X| / (254 q_max), one correctly rounded division.
-  double tmax = 0.0;
-  for (double v : chmax) tmax = std::max(tmax, v);
-  if (!(tmax > 0.0)) return fail(MM_ERR_DEGENERATE, "calibration data has max|X| == 0");
-  const double t4 = (std::ldexp(1.0, bias_of(F_E2M1) + 4 - 1) * tmax) / (254.0 * qmax_of(F_E2M1));
-  const double t6 = (std::ldexp(1.0, bias_of(fmt6) + 6 - 1) * tmax) / (254.0 * qmax_of(fmt6));
-  // Eq. 6 / Eq. 17: channel counts by channel max.
-  int32_t c4 = 0, c6 = 0;
-  for (double v : chmax) {
-    if (v <= t4) ++c4;
-    else if (v <= t6) ++c6;
-  }
-  const int32_t c8 = K - c4 - c6;
-  // Rounding to whole 32-blocks: n8 up, then n6 up (capped), n4 the remainder.
-  int32_t n[3];
-  n[2] = (int32_t)roundup(c8, 32);
-  n[1] = std::min((int32_t)roundup(c6, 32), K - n[2]);
-  n[0] = K - n[2] - n[1];
-  // Eq. 7 + Q3: stable ascending argsort of the channel means.
-  std::vector<int32_t> perm(K);
-  std::iota(perm.begin(), perm.end(), 0);
-  std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return chmean[a] < chmean[b]; });
-  if ((st = mm_plan_init(plan_out, K, n, fmt6, fmt8, rule, perm.data(), d_perm_out, stream)) != MM_OK) return st;
-  plan_out->tensor_max = tmax;
-  plan_out->t4 = t4;
-  plan_out->t6 = t6;
-  plan_out->c[0] = c4;
-  plan_out->c[1] = c6;
-  plan_out->c[2] = c8;
+  if ((st = plan_from_stats(chmax, chmean, K, fmt6, fmt8, rule, d_perm_out, plan_out, stream)) != MM_OK) return st;
   if (h_chmax) std::memcpy(h_chmax, chmax.data(), (size_t)K * 8);
   if (h_chmean) std::memcpy(h_chmean, chmean.data(), (size_t)K * 8);
+  return MM_OK;
+}
+
+int64_t mm_calib_state_bytes(int32_t K) { return K <= 0 ? -1 : (int64_t)calib_state_bytes(K); }
+
+mm_status mm_calib_accumulate(const void* d_x, int64_t L, int32_t K, int64_t ldx, void* d_ws, size_t ws_bytes,
+                              void* d_state, mm_stream_t stream) {
+  mm_status st = check_device();
+  if (st != MM_OK) return st;
+  if (K < 32 || K % 32 != 0 || K > 65536) return fail(MM_ERR_SHAPE, "K=%d must be a multiple of 32 in [32, 65536]", K);
+  if (!d_x || !d_ws || !d_state) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (L <= 0) return fail(MM_ERR_SHAPE, "L must be positive");
+  if (ldx < K) return fail(MM_ERR_SHAPE, "ldx < K");
+  if (ldx % 8 != 0 || !aligned(d_x, 16)) return fail(MM_ERR_ALIGNMENT, "input rows must be 16-byte aligned");
+  if (!aligned(d_state, 256)) return fail(MM_ERR_ALIGNMENT, "state must be 256-byte aligned");
+  if ((int64_t)ws_bytes < mm_calib_workspace_bytes(L, K) || !aligned(d_ws, 256))
+    return fail(MM_ERR_WORKSPACE, "workspace too small or unaligned (need %lld bytes)",
+                (long long)mm_calib_workspace_bytes(L, K));
+  cudaError_t e = launch_calib_accumulate(static_cast<const uint16_t*>(d_x), L, ldx, K, d_ws, d_state,
+                                          reinterpret_cast<cudaStream_t>(stream), &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "calibration accumulate launch");
+  return MM_OK;
+}
+
+mm_status mm_calib_finalize(const void* d_state, int32_t K, int32_t fmt6, int32_t fmt8, int32_t rule,
+                            int32_t* d_perm_out, mm_plan* plan_out, double* h_chmax, double* h_chmean,
+                            int64_t* h_rows, mm_stream_t stream) {
+  mm_status st = check_device();
+  if (st != MM_OK) return st;
+  const int32_t nz[3] = {K, 0, 0};
+  if ((st = validate_plan_fields(K, nz, fmt6, fmt8, rule)) != MM_OK) return st;
+  if (!d_state || !d_perm_out || !plan_out) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  std::vector<uint8_t> h(calib_state_bytes(K));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(h.data(), d_state, h.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "calibration state");
+  std::vector<double> chmax(K), chmean(K);
+  int64_t rows = 0;
+  calib_state_to_stats(h.data(), K, chmax.data(), chmean.data(), &rows);
+  if (rows <= 0) return fail(MM_ERR_DEGENERATE, "no calibration rows accumulated");
+  if ((st = plan_from_stats(chmax, chmean, K, fmt6, fmt8, rule, d_perm_out, plan_out, stream)) != MM_OK) return st;
+  if (h_chmax) std::memcpy(h_chmax, chmax.data(), (size_t)K * 8);
+  if (h_chmean) std::memcpy(h_chmean, chmean.data(), (size_t)K * 8);
+  if (h_rows) *h_rows = rows;
+  return MM_OK;
+}
+
+mm_status mm_plan_diagnostics(const mm_plan* plan, const double* h_chmax, const int32_t* h_perm,
+                              mm_plan_diag* out) {
+  if (!plan || !out) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  mm_status st = validate_plan_fields(plan->K, plan->n, plan->fmt6, plan->fmt8, plan->rule);
+  if (st != MM_OK) return st;
+  const int32_t K = plan->K;
+  std::memset(out, 0, sizeof(*out));
+  for (int g = 0; g < 3; ++g) out->p[g] = (double)plan->n[g] / K;
+  // Table 1 accounting: element bits + 8-bit E8M0 scale per 32 elements
+  out->avg_bits = (4.0 * plan->n[0] + 6.0 * plan->n[1] + 8.0 * plan->n[2]) / K + 8.0 / 32.0;
+  out->stored_bytes_per_row = 0;
+  for (int g = 0; g < 3; ++g) out->stored_bytes_per_row += mm_code_pitch_bytes(plan, g) + roundup(plan->n[g], 128) / 32;
+  if (h_chmax && h_perm && plan->t4 > 0.0) {
+    // Eq. 6 violations: channels ordered by mean (Eq. 7) into a group whose threshold
+    // their maximum exceeds (a diagnostic, never "fixed": DESIGN.md R13)
+    for (int32_t j = 0; j < plan->n[0]; ++j) out->eq6_violations[0] += h_chmax[h_perm[j]] > plan->t4;
+    for (int32_t j = plan->n[0]; j < plan->n[0] + plan->n[1]; ++j)
+      out->eq6_violations[1] += h_chmax[h_perm[j]] > plan->t6;
+  }
   return MM_OK;
 }
 

@@ -83,3 +83,26 @@ def test_shard_rows_host_logic():
     assert mm.shard_rows(8192, 8, 3) == (3072, 4096)
     with pytest.raises(ValueError):
         mm.shard_rows(100, 8, 0)
+
+
+def test_plan_diagnostics_host(L):
+    """mm_plan_diagnostics is host-only: p, Table-1 average bits, stored bytes per row
+    and Eq. 6 violations against the oracle's own accounting."""
+    import numpy as np
+    from oracle import calib as ocal
+    from synth import bf16_bits, gen_act
+    K = 512
+    cal = ocal.calibrate(bf16_bits(gen_act(300, K, 1000, 2000)))
+    c = _plan(K, cal["n"])
+    c.t4, c.t6 = cal["t4"], cal["t6"]
+    chmax = np.ascontiguousarray(cal["chmax"], dtype=np.float64)
+    perm = np.ascontiguousarray(cal["perm"], dtype=np.int32)
+    d = mm.CDiag()
+    st = L.mm_plan_diagnostics(ctypes.byref(c), ctypes.c_void_p(chmax.ctypes.data), ctypes.c_void_p(perm.ctypes.data),
+                               ctypes.byref(d))
+    assert st == 0
+    assert abs(d.avg_bits - ocal.avg_bits(cal["n"])) < 1e-12
+    assert tuple(d.eq6_violations) == ocal.eq6_violations(cal["perm"], cal["n"], cal["chmax"], cal["t4"], cal["t6"])
+    assert [round(v * K) for v in d.p] == list(cal["n"])
+    pitch = [(n + 127) // 128 * 128 * b // 8 for n, b in zip(cal["n"], (4, 6, 8))]
+    assert d.stored_bytes_per_row == sum(pitch) + sum((n + 127) // 128 * 4 for n in cal["n"])

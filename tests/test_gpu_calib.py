@@ -44,3 +44,24 @@ def test_degenerate_raises():
     with pytest.raises(mm.MMError) as e:
         mm.mm_calibrate_thresholds(torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda"))
     assert e.value.status == 5
+
+
+def test_streaming_calibration_equals_one_shot():
+    """mm_calib_accumulate over three batches + mm_calib_finalize == the oracle's
+    calibration of the concatenated rows (pooled statistics, R15)."""
+    K = 1024
+    xs = [gen_act(L, K, 1000, 2000 + i) for i, L in enumerate((700, 1500, 33))]
+    st = mm.CalibState(K)
+    for x in xs:
+        st.accumulate(x.cuda())
+    plan, chmax, chmean, rows = st.finalize(return_stats=True)
+    assert rows == sum(x.shape[0] for x in xs)
+    ref = ocal.calibrate(np.concatenate([bf16_bits(x) for x in xs]))
+    assert plan.n == ref["n"]
+    assert np.array_equal(plan.perm_host().numpy(), ref["perm"])
+    assert np.array_equal(chmax.numpy(), ref["chmax"])
+    assert plan.c.t4 == ref["t4"] and plan.c.t6 == ref["t6"]
+    d = mm.mm_plan_diagnostics(plan, chmax)
+    assert abs(d["avg_bits"] - ocal.avg_bits(plan.n)) < 1e-12
+    v4, v6 = ocal.eq6_violations(ref["perm"], ref["n"], ref["chmax"], ref["t4"], ref["t6"])
+    assert d["eq6_violations"] == (v4, v6)
