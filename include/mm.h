@@ -177,6 +177,18 @@ mm_status mm_reorder_quantize_act(const void* d_x, int64_t M, int64_t ldx,
                                   const mm_plan* plan, mm_mx_tensor* a_out,
                                   mm_stream_t stream);
 
+/* RMSNorm fused into the online reorder-and-quantize (the paper's integration: one
+ * RQ after each normalization layer, shared by the following linears, §3.2 / Fig. 7
+ * lines 156-163).  Quantizes y = RMSNorm(X) * gamma, where for
+ * every row ss = sum_j x_j^2 (exact), r = fp32(1 / sqrt(ss / K + eps)) (IEEE fp64),
+ * t_j = bf16_rne(fp32(x_j * r)) and y_j = bf16_rne(fp32(gamma_j * t_j)) (the HF
+ * LlamaRMSNorm data flow; reading R27) -- bit-exact with quantizing the
+ * separately normalized BF16 rows.  d_gamma: device BF16[K] in the
+ * ORIGINAL channel order, 16-byte aligned; eps > 0.  Saves the BF16 write and read of
+ * the normalized activation. */
+mm_status mm_rmsnorm_reorder_quantize_act(const void* d_x, int64_t M, int64_t ldx, const void* d_gamma, double eps,
+                                          const mm_plan* plan, mm_mx_tensor* a_out, mm_stream_t stream);
+
 /* Mixed block-scaled GEMM (§3.2, Eq. 2): Y[M, N] = A W^T over the three
  * K-segments, one FP32 accumulator, BF16 round-to-nearest-even output
  * (row-major, ld = ldy >= N, ldy % 8 == 0).  A and W must come from `plan`

@@ -7,11 +7,14 @@ the norm into the RQ kernel.  The paper does not define the norm's arithmetic;
 DESIGN.md reading R27 fixes it so that one exact answer exists:
 
     ss_m  = sum_j x_mj^2                      exact, then rounded once to fp64
-    r_m   = 1 / sqrt(ss_m / K + eps)          IEEE fp64 division and square root
-    y_mj  = bf16_rne( (x_mj * gamma_j) * r_m ) the product x*gamma is exact in fp64
-                                               (8-bit significands), the multiply
-                                               by r_m rounds once in fp64, then one
-                                               round-to-nearest-even to BF16
+    r_m   = fp32( 1 / sqrt(ss_m / K + eps) )  IEEE fp64 division and square root,
+                                               rounded once to fp32
+    t_mj  = bf16_rne( fp32(x_mj * r_m) )      normalised activation in BF16
+    y_mj  = bf16_rne( fp32(gamma_j * t_mj) )  weight applied to the BF16 value
+
+i.e. the HF LlamaRMSNorm data flow (fp32 normalise, cast to BF16, multiply by the
+BF16 weight) with the row's sum of squares taken exactly, so that the result does
+not depend on a reduction order.
 
 and the quantized operand is reorder_quantize(y) (oracle/mx.py).
 """
@@ -37,17 +40,22 @@ def exact_sumsq(x_row_bits: np.ndarray) -> float:
     return float(tot)                               # Fraction -> float is correctly rounded
 
 
+def row_scale_f32(x_row_bits, K: int, eps: float) -> np.float32:
+    """r = fp32(1 / sqrt(exact_sumsq / K + eps)) (fp64 arithmetic, one fp32 rounding)."""
+    return np.float32(1.0 / np.sqrt(exact_sumsq(x_row_bits) / K + eps))
+
+
 def rmsnorm_bf16_bits(x_bits: np.ndarray, gamma_bits: np.ndarray, eps: float) -> np.ndarray:
     """y = RMSNorm(x) * gamma as BF16 bit patterns [rows, K] (definition above)."""
     x_bits = np.asarray(x_bits, dtype=np.uint16)
     rows, K = x_bits.shape
-    x = bf16_to_f64(x_bits)
-    g = bf16_to_f64(np.asarray(gamma_bits, dtype=np.uint16))
+    x = bf16_to_f64(x_bits).astype(np.float32)                      # exact
+    g = bf16_to_f64(np.asarray(gamma_bits, dtype=np.uint16)).astype(np.float32)
     out = np.empty_like(x_bits)
     for i in range(rows):
-        ss = exact_sumsq(x_bits[i])
-        r = 1.0 / np.sqrt(ss / K + eps)
-        out[i] = bf16_rne_bits((x[i] * g) * r)
+        r = row_scale_f32(x_bits[i], K, eps)
+        t = bf16_rne((x[i] * r).astype(np.float64))                    # fp32 multiply, BF16 RNE
+        out[i] = bf16_rne_bits((g * t.astype(np.float32)).astype(np.float64))
     return out
 
 
@@ -62,4 +70,4 @@ def rmsnorm_f64(x_bits, gamma_bits, eps):
     return out
 
 
-__all__ = ["exact_sumsq", "rmsnorm_bf16_bits", "rmsnorm_f64", "bf16_rne"]
+__all__ = ["exact_sumsq", "row_scale_f32", "rmsnorm_bf16_bits", "rmsnorm_f64", "bf16_rne"]

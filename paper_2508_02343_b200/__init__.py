@@ -36,6 +36,7 @@ EXPORTS = [
     "mm_last_error", "mm_abi_version", "mm_nccl_unique_id_bytes", "mm_nccl_get_unique_id",
     "mm_comm_init", "mm_comm_destroy", "mm_mixed_gemm_bf16_nshard_allgather",
     "mm_calib_state_bytes", "mm_calib_accumulate", "mm_calib_finalize", "mm_plan_diagnostics",
+    "mm_rmsnorm_reorder_quantize_act",
 ]
 
 
@@ -107,6 +108,7 @@ def lib(build_if_missing: bool = False):
             "mm_calib_accumulate": (ctypes.c_int, [vp, i64, i32, i64, vp, ctypes.c_size_t, vp, vp]),
             "mm_calib_finalize": (ctypes.c_int, [vp, i32, i32, i32, i32, vp, P, vp, vp, vp, vp]),
             "mm_plan_diagnostics": (ctypes.c_int, [P, vp, vp, ctypes.POINTER(CDiag)]),
+            "mm_rmsnorm_reorder_quantize_act": (ctypes.c_int, [vp, i64, i64, vp, ctypes.c_double, P, X, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -282,6 +284,19 @@ def mm_quantize_weight_offline(w: torch.Tensor, plan: Plan, out: MXTensor | None
 
 def mm_reorder_quantize_act(x: torch.Tensor, plan: Plan, out: MXTensor | None = None, stream=None):
     return _rq(lib().mm_reorder_quantize_act, x, plan, out, stream)
+
+
+def mm_rmsnorm_reorder_quantize_act(x: torch.Tensor, gamma: torch.Tensor, eps: float, plan: Plan,
+                                    out: MXTensor | None = None, stream=None) -> MXTensor:
+    """RMSNorm(x) * gamma, reordered and quantized in one kernel (F2 fusion)."""
+    assert x.dtype == torch.bfloat16 and x.dim() == 2 and x.stride(1) == 1
+    assert gamma.dtype == torch.bfloat16 and gamma.is_contiguous() and gamma.numel() == x.shape[1]
+    rows = x.shape[0]
+    if out is None:
+        out = MXTensor(plan, rows, x.device)
+    _check(lib().mm_rmsnorm_reorder_quantize_act(_ptr(x), rows, x.stride(0), _ptr(gamma), float(eps),
+                                                 ctypes.byref(plan.c), ctypes.byref(out.c), _stream(stream)))
+    return out
 
 
 def mm_mixed_gemm_bf16(a: MXTensor, w: MXTensor, plan: Plan, out: torch.Tensor | None = None,

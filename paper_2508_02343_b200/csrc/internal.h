@@ -31,6 +31,8 @@ struct RqArgs {
   SegGeom geom;
   uint8_t* codes[3];
   uint8_t* sf[3];
+  const uint16_t* gamma;  // BF16 [K] RMSNorm weight, or nullptr (no norm; F2 fusion)
+  double eps;             // RMSNorm epsilon (> 0) when gamma != nullptr
 };
 
 // Fused reorder-and-quantize (rq.cu).

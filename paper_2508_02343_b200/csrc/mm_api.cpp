@@ -162,7 +162,7 @@ mm_status check_mx_out(const mm_plan* p, const mm_mx_tensor* t, int64_t rows, co
 }
 
 mm_status run_rq(const void* d_x, int64_t rows, int64_t ldx, const mm_plan* plan, mm_mx_tensor* out,
-                 mm_stream_t stream, const char* what) {
+                 mm_stream_t stream, const char* what, const void* d_gamma = nullptr, double eps = 0.0) {
   mm_status st = check_device();
   if (st != MM_OK) return st;
   if ((st = validate_plan(plan)) != MM_OK) return st;
@@ -182,6 +182,8 @@ mm_status run_rq(const void* d_x, int64_t rows, int64_t ldx, const mm_plan* plan
   a.K = plan->K;
   a.perm = plan->d_perm;
   a.geom = geom_of(plan);
+  a.gamma = static_cast<const uint16_t*>(d_gamma);
+  a.eps = eps;
   for (int g = 0; g < 3; ++g) {
     a.codes[g] = static_cast<uint8_t*>(out->codes[g]);
     a.sf[g] = static_cast<uint8_t*>(out->sf[g]);
@@ -448,6 +450,14 @@ mm_status mm_quantize_weight_offline(const void* d_w, int64_t N, int64_t ldw, co
 mm_status mm_reorder_quantize_act(const void* d_x, int64_t M, int64_t ldx, const mm_plan* plan, mm_mx_tensor* a_out,
                                   mm_stream_t stream) {
   return run_rq(d_x, M, ldx, plan, a_out, stream, "a_out");
+}
+
+mm_status mm_rmsnorm_reorder_quantize_act(const void* d_x, int64_t M, int64_t ldx, const void* d_gamma, double eps,
+                                          const mm_plan* plan, mm_mx_tensor* a_out, mm_stream_t stream) {
+  if (!d_gamma) return fail(MM_ERR_INVALID_ARGUMENT, "gamma is NULL");
+  if (!(eps > 0.0) || !std::isfinite(eps)) return fail(MM_ERR_INVALID_ARGUMENT, "eps must be finite and > 0");
+  if (!aligned(d_gamma, 16)) return fail(MM_ERR_ALIGNMENT, "gamma must be 16-byte aligned");
+  return run_rq(d_x, M, ldx, plan, a_out, stream, "a_out", d_gamma, eps);
 }
 
 mm_status mm_reorder_act_bf16(const void* d_x, int64_t M, int64_t ldx, const mm_plan* plan, void* d_xr,

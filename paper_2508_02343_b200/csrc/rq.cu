@@ -181,6 +181,62 @@ __device__ __forceinline__ void encode_store(const ST (&v)[NV], float inv, uint8
   }
 }
 
+// ---- fused RMSNorm (reading R27) ----------------------
+template <int RHO> __device__ __forceinline__ uint32_t slot_bits(const uint16_t& s) { return s; }
+template <int RHO> __device__ __forceinline__ uint32_t slot_bits(const uint32_t& s) { return (s >> (16 * RHO)) & 0xFFFFu; }
+template <int RHO> __device__ __forceinline__ uint32_t slot_bits(const uint2& s) {
+  return ((RHO < 2 ? s.x : s.y) >> (16 * (RHO & 1))) & 0xFFFFu;
+}
+__device__ __forceinline__ void slot_pack(uint16_t& s, const uint32_t (&b)[4]) { s = (uint16_t)b[0]; }
+__device__ __forceinline__ void slot_pack(uint32_t& s, const uint32_t (&b)[4]) { s = b[0] | (b[1] << 16); }
+__device__ __forceinline__ void slot_pack(uint2& s, const uint32_t (&b)[4]) {
+  s = make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
+}
+__device__ __forceinline__ double bf16_f64(uint32_t b) { return (double)__uint_as_float(b << 16); }
+// double-double accumulation (TwoSum): exact sums of squares of BF16 values
+__device__ __forceinline__ void dd_add(double& hi, double& lo, double v) {
+  const double s = hi + v, bb = s - hi;
+  lo += (hi - (s - bb)) + (v - bb);
+  hi = s;
+}
+__device__ __forceinline__ void dd_add_dd(double& hi, double& lo, double bhi, double blo) {
+  const double s = hi + bhi, bb = s - hi;
+  double err = (hi - (s - bb)) + (bhi - bb);
+  err += lo + blo;
+  hi = s + err;
+  lo = err - (hi - s);
+}
+// t = bf16_rne(fp32(x * r)), y = bf16_rne(fp32(gamma * t)) for every row of a slot
+// (reading R27: the HF LlamaRMSNorm data flow), packed fp32x2 multiplies
+// and bf16x2 conversions (RNE, no flush of subnormals).
+__device__ __forceinline__ uint32_t bf16x2_rne(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t norm_pair(uint32_t w, float g, float r0, float r1) {
+  const float2 p = __fmul2_rn(make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)),
+                              make_float2(r0, r1));
+  const uint32_t t = bf16x2_rne(p.x, p.y);
+  const float2 q = __fmul2_rn(make_float2(__uint_as_float(t << 16), __uint_as_float(t & 0xFFFF0000u)),
+                              make_float2(g, g));
+  return bf16x2_rne(q.x, q.y);
+}
+template <int R>
+__device__ __forceinline__ void norm_slot(uint16_t& v, uint32_t gbits, const float (&r)[4]) {
+  const float g = __uint_as_float(gbits << 16);
+  v = (uint16_t)norm_pair(v, g, r[0], r[0]);
+}
+template <int R>
+__device__ __forceinline__ void norm_slot(uint32_t& v, uint32_t gbits, const float (&r)[4]) {
+  v = norm_pair(v, __uint_as_float(gbits << 16), r[0], r[1]);
+}
+template <int R>
+__device__ __forceinline__ void norm_slot(uint2& v, uint32_t gbits, const float (&r)[4]) {
+  const float g = __uint_as_float(gbits << 16);
+  v = make_uint2(norm_pair(v.x, g, r[0], r[1]), norm_pair(v.y, g, r[2], r[3]));
+}
+
 // Block amax of each of the R rows over |bf16| bits (packed 16x2 maxima).  With
 // NV = 16 each lane holds half a block; the lane pair combines with one shuffle.
 template <int NV>
@@ -272,8 +328,8 @@ struct RqDev {
 //    channel that returns all R rows (the permutation is read through L1 as
 //    16-byte vectors), block amax, scale and encode as above; finally the stage
 //    is released to the producer.
-template <int R>
-__global__ void __launch_bounds__(R == 4 ? 704 : 1024, 1)
+template <int R, bool NORM>
+__global__ void __launch_bounds__((R == 4 || NORM) ? 704 : 1024, 1)
 rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev d) {
   using ST = typename Slot<R>::T;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -287,7 +343,13 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   const size_t tab_bytes = d.perm_smem ? (size_t)K * 4 + (size_t)16 * (K / 32 + 1) * 4 : 0;
   const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
   uint32_t* gidx = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + (size_t)K * 4);   // 16 x nblk_s words
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)d.stages * stage_bytes + tab_bytes);
+  // optional RMSNorm region: gamma in reordered order (K x u16) + reduction scratch
+  constexpr bool norm = NORM;   // RMSNorm fused ahead of the quantization (a.gamma != nullptr)
+  const size_t norm_bytes = norm ? ((size_t)K * 2 + 255) / 256 * 256 + 4096 : 0;
+  uint16_t* gamma_r = reinterpret_cast<uint16_t*>(smem + (size_t)d.stages * stage_bytes + tab_bytes);
+  double* nred = reinterpret_cast<double*>(smem + (size_t)d.stages * stage_bytes + tab_bytes +
+                                           ((size_t)K * 2 + 255) / 256 * 256);   // [3 grp][..]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)d.stages * stage_bytes + tab_bytes + norm_bytes);
   uint64_t* empty = full + d.stages;
   uint64_t* permbar = empty + d.stages;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -368,6 +430,15 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     if ((d.dbg & 32) && threadIdx.x == 32) g_rq_trace[blockIdx.x][1] = ptx::globaltimer_ns();
   }
   ptx::grid_dep_wait();   // the outputs may still be read by the preceding kernel
+  if constexpr (NORM) {   // gamma in reordered channel order
+    const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
+    for (int j = ct; j < K; j += cn) {
+      const int pj = use_tab ? perm_s[j] : __ldg(a.perm + j);
+      gamma_r[j] = __ldg(a.gamma + pj);
+    }
+    ptx::named_bar_sync(15, cn);
+  }
+  const double eps = a.eps;
   // Work is split into chunks of 16 consecutive blocks of ONE segment (a warp's
   // lanes never mix segments, so the encode path is warp-uniform); the two lanes of
   // a pair share a block, 16 channels each.
@@ -410,6 +481,42 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     // ---- gather + quantize + pack + store ----
     if (dbg & 3) { __syncwarp(); if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s])); continue; }
     const ST* slots = reinterpret_cast<const ST*>(st);
+    float rn[4] = {0.f, 0.f, 0.f, 0.f};
+    if constexpr (NORM) {
+      // exact per-row sums of squares (double-double), group reduction in a fixed order
+      double hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+      for (int pc = gw * 32 + lane; pc < K; pc += gthreads) {
+        const ST v = slots[pc];
+        { const double x = bf16_f64(slot_bits<0>(v)); dd_add(hi[0], lo[0], x * x); }
+        if constexpr (R >= 2) { const double x = bf16_f64(slot_bits<1>(v)); dd_add(hi[1], lo[1], x * x); }
+        if constexpr (R >= 4) {
+          { const double x = bf16_f64(slot_bits<2>(v)); dd_add(hi[2], lo[2], x * x); }
+          { const double x = bf16_f64(slot_bits<3>(v)); dd_add(hi[3], lo[3], x * x); }
+        }
+      }
+#pragma unroll
+      for (int rho = 0; rho < R; ++rho)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double oh = __shfl_xor_sync(0xffffffffu, hi[rho], o), ol = __shfl_xor_sync(0xffffffffu, lo[rho], o);
+          dd_add_dd(hi[rho], lo[rho], oh, ol);
+        }
+      // scratch: [consumer warp (<= 31)][rho][hi, lo] doubles, then [group][rho] norms
+      double* red = nred + (grp * group_warps) * 8;
+      if (lane == 0)
+#pragma unroll
+        for (int rho = 0; rho < R; ++rho) { red[gw * 8 + 2 * rho] = hi[rho]; red[gw * 8 + 2 * rho + 1] = lo[rho]; }
+      ptx::named_bar_sync(1 + grp, gthreads);
+      if (gw == 0 && lane < R) {
+        double h2 = 0.0, l2 = 0.0;
+        for (int ww = 0; ww < group_warps; ++ww) dd_add_dd(h2, l2, red[ww * 8 + 2 * lane], red[ww * 8 + 2 * lane + 1]);
+        const double ss = h2 + l2;
+        nred[32 * 8 + grp * 4 + lane] = (double)(float)(1.0 / sqrt(ss / (double)K + eps));   // fp32 row scale
+      }
+      ptx::named_bar_sync(1 + grp, gthreads);
+#pragma unroll
+      for (int rho = 0; rho < R; ++rho) rn[rho] = (float)nred[32 * 8 + grp * 4 + rho];
+    }
     const int64_t r0 = (blockIdx.x + i * gridDim.x) * (int64_t)R;
     const int64_t left = rows - r0;
     const int nvalid = left >= R ? R : (left > 0 ? (int)left : 0);
@@ -460,6 +567,13 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
           v[4 * q + 3] = slots[pv.w];
         }
       }
+      if constexpr (NORM) {
+        const uint4* gp4 = reinterpret_cast<const uint4*>(gamma_r + off_g + 32 * kb + 16 * h);
+        const uint4 ga = gp4[0], gb = gp4[1];
+        const uint32_t gw8[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) norm_slot<R>(v[i], (gw8[i >> 1] >> (16 * (i & 1))) & 0xFFFFu, rn);
+      }
       const bool sf_lane = h == 0;
       if (g == 0) quantize_tile_block<R, 0, F_E2M1, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
       else if (g == 1) {
@@ -485,7 +599,7 @@ __global__ void reorder_bf16_kernel(const uint16_t* __restrict__ x, int64_t rows
     xr[r * ldxr + j] = x[r * ldx + perm[j]];
 }
 
-template <int R>
+template <int R, bool NORM>
 cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   EncodeTiledFn enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
@@ -499,7 +613,8 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   const size_t tab_need = (size_t)a.K * 4 + (size_t)16 * (a.K / 32 + 1) * 4;   // perm copy + gather table
   d.perm_smem = (200 * 1024 - tab_need) / stage_bytes >= 3 ? 1 : 0;
   const size_t tab_bytes = d.perm_smem ? tab_need : 0;
-  int stages = (int)((200 * 1024 - tab_bytes) / stage_bytes);
+  const size_t norm_need = a.gamma ? ((size_t)a.K * 2 + 255) / 256 * 256 + 4096 : 0;
+  int stages = (int)((200 * 1024 - tab_bytes - norm_need) / stage_bytes);
   if (stages > 8) stages = 8;
   { const char* e = getenv("MM_RQ_STAGES"); if (e && atoi(e) >= 2 && atoi(e) < stages) stages = atoi(e); }
   if (stages < 2) return cudaErrorInvalidConfiguration;
@@ -508,7 +623,7 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   if (gw > 12) gw = 12;
   if (gw < 2) gw = 2;
   d.group_warps = gw;
-  int groups = (R == 4 ? 21 : 31) / gw;   // consumer warps (+ the producer warp) within the register budget
+  int groups = ((R == 4 || NORM) ? 21 : 31) / gw;   // consumer warps (+ the producer warp) within the register budget
   if (groups > stages - 1) groups = stages - 1;
   if (groups < 1) groups = 1;
   d.groups = groups;
@@ -539,13 +654,14 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + tab_bytes + (2 * stages + 1) * 8;
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(rq_kernel<R>), smem);
+  const size_t norm_bytes = a.gamma ? ((size_t)a.K * 2 + 255) / 256 * 256 + 4096 : 0;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + tab_bytes + norm_bytes + (2 * stages + 1) * 8;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(rq_kernel<R, NORM>), smem);
   if (e != cudaSuccess) return e;
   const int threads = 32 * (1 + groups * gw);
   int64_t grid = sm_count();
   if (grid > d.n_tiles) grid = d.n_tiles;
-  e = launch_pdl(rq_kernel<R>, dim3((unsigned)grid), dim3(threads), smem, s, m, d);
+  e = launch_pdl(rq_kernel<R, NORM>, dim3((unsigned)grid), dim3(threads), smem, s, m, d);
   if (launches) ++*launches;
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -556,14 +672,14 @@ cudaError_t launch_reorder_quantize(const RqArgs& a, cudaStream_t s, int64_t* la
   if (a.rows == 0) return cudaSuccess;
   const size_t row_bytes = (size_t)((a.K + 255) / 256) * 512;
   static const int force_r = [] { const char* e = getenv("MM_RQ_ROWS"); return e ? atoi(e) : 0; }();  // tuning
-  if (force_r == 2) return launch_rq_t<2>(a, s, launches);
-  if (force_r == 1) return launch_rq_t<1>(a, s, launches);
-  if (force_r == 4) return launch_rq_t<4>(a, s, launches);
+  if (force_r == 2) return (a.gamma ? launch_rq_t<2, true>(a, s, launches) : launch_rq_t<2, false>(a, s, launches));
+  if (force_r == 1) return (a.gamma ? launch_rq_t<1, true>(a, s, launches) : launch_rq_t<1, false>(a, s, launches));
+  if (force_r == 4) return (a.gamma ? launch_rq_t<4, true>(a, s, launches) : launch_rq_t<4, false>(a, s, launches));
   // Two-row tiles while >= 3 stages fit (measured faster than four-row tiles at
   // q_proj: twice the tiles balance the persistent grid, fewer registers per lane
   // allow more consumer warps), single rows beyond.
-  if (2 * row_bytes * 3 <= 200 * 1024) return launch_rq_t<2>(a, s, launches);
-  return launch_rq_t<1>(a, s, launches);
+  if (2 * row_bytes * 3 <= 200 * 1024) return (a.gamma ? launch_rq_t<2, true>(a, s, launches) : launch_rq_t<2, false>(a, s, launches));
+  return (a.gamma ? launch_rq_t<1, true>(a, s, launches) : launch_rq_t<1, false>(a, s, launches));
 }
 
 }  // namespace mmx

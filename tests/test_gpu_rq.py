@@ -148,3 +148,33 @@ def test_errors_are_loud():
     with pytest.raises(mm.MMError) as e:
         mm.mm_mixed_gemm_bf16(a, w, plan)
     assert e.value.status == 4
+
+
+@pytest.mark.parametrize("M,K,n,eps", [(16, 256, (128, 64, 64), 1e-5), (300, 4096, (2240, 1184, 672), 1e-6),
+                                       (77, 14336, (8512, 3840, 1984), 1e-5)])
+def test_rmsnorm_fused_bit_exact(M, K, n, eps):
+    """F2: RMSNorm fused into the RQ == the oracle's norm (reading R27) followed by the
+    oracle's reorder-quantize, bit for bit (codes, scales, padding)."""
+    from oracle import norm as onorm
+    from synth import gen_uniform_bf16
+    plan = _fixed_plan(K, n, seed=9)
+    x = gen_act(M, K, 1000, 2700 + M)
+    gamma = gen_uniform_bf16((K,), 0.1, 3.0, 11)
+    q = mm.mm_rmsnorm_reorder_quantize_act(x.cuda(), gamma.cuda(), eps, plan)
+    torch.cuda.synchronize()
+    y_bits = onorm.rmsnorm_bf16_bits(bf16_bits(x), bf16_bits(gamma), eps)
+    codes, scales, pads = decode_operand(q, plan.n)
+    oc, osf, _ = omx.reorder_quantize(y_bits, plan.perm_host().numpy(), plan.n)
+    for g in range(3):
+        assert np.array_equal(codes[g], oc[g]), f"codes seg {g}: {np.argwhere(codes[g] != oc[g])[:5]}"
+        assert np.array_equal(scales[g], osf[g]), f"scales seg {g}"
+        cpad, spad_c, spad_r = pads[g]
+        assert not np.any(cpad) and not np.any(spad_c) and not np.any(spad_r)
+
+
+def test_rmsnorm_rejects_bad_eps():
+    plan = _fixed_plan(256, (128, 64, 64), seed=10)
+    x = gen_act(8, 256, 1006, 2500).cuda()
+    g = torch.ones(256, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(mm.MMError):
+        mm.mm_rmsnorm_reorder_quantize_act(x, g, 0.0, plan)
