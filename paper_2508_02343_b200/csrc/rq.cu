@@ -310,7 +310,7 @@ struct RqDev {
   int64_t n_tiles;      // tiles of R rows covering roundup(rows, 128)
   int nbox;             // TMA boxes of 256 channels per row
   int stages, groups, group_warps;
-  int perm_smem;        // 1: permutation staged in smem as a gather table, 0: read through L1
+  int perm_smem;        // 1: perm copied by bulk copy + gather table, 2: gather table built from global, 0: L1
   int box3d;            // 1: one 3-D TMA per tile ({256, R, nbox} box), 0: nbox 2-D boxes
   int dbg;              // timing experiments only (env MM_RQ_DEBUG): 1 = skip gather/quantize, 2 = skip transpose too
 };
@@ -340,9 +340,10 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   const int stage_bytes = d.nbox * 512 * R;
   // [ring of stages][perm copy: K x int32][gather table: K x u16][barriers]
   const int K = a.K, nblk = K / 32, nblk_s = nblk + 1;   // table row stride padded (bank spread)
-  const size_t tab_bytes = d.perm_smem ? (size_t)K * 4 + (size_t)16 * (K / 32 + 1) * 4 : 0;
+  const size_t perm_copy = d.perm_smem == 1 ? (size_t)K * 4 : 0;
+  const size_t tab_bytes = d.perm_smem ? perm_copy + (size_t)16 * (K / 32 + 1) * 4 : 0;
   const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
-  uint32_t* gidx = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + (size_t)K * 4);   // 16 x nblk_s words
+  uint32_t* gidx = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + perm_copy);   // 16 x nblk_s words
   // optional RMSNorm region: gamma in reordered order (K x u16) + reduction scratch
   constexpr bool norm = NORM;   // RMSNorm fused ahead of the quantization (a.gamma != nullptr)
   const size_t norm_bytes = norm ? ((size_t)K * 2 + 255) / 256 * 256 + 4096 : 0;
@@ -363,7 +364,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     ptx::mbar_init(ptx::smem_u32(permbar), 1);
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tmx);
-    if (d.perm_smem) {  // the permutation arrives asynchronously, alongside the first tiles
+    if (d.perm_smem == 1) {  // the permutation arrives asynchronously, alongside the first tiles
       ptx::mbar_arrive_expect_tx(ptx::smem_u32(permbar), (uint32_t)K * 4);
       ptx::bulk_load(ptx::smem_u32(perm_s), a.perm, (uint32_t)K * 4, ptx::smem_u32(permbar));
     }
@@ -419,11 +420,12 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   // the lanes of a warp (consecutive blocks) read consecutive words.
   const bool use_tab = d.perm_smem != 0;
   if (use_tab) {
-    ptx::mbar_wait(ptx::smem_u32(permbar), 0, 13, 0, 0);
+    if (d.perm_smem == 1) ptx::mbar_wait(ptx::smem_u32(permbar), 0, 13, 0, 0);
     const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
     for (int t = ct; t < K / 2; t += cn) {
       const int blk = t >> 4, i2 = t & 15;
-      const uint2 pr = *reinterpret_cast<const uint2*>(perm_s + 32 * blk + 2 * i2);
+      const uint2 pr = d.perm_smem == 1 ? *reinterpret_cast<const uint2*>(perm_s + 32 * blk + 2 * i2)
+                                        : __ldg(reinterpret_cast<const uint2*>(a.perm + 32 * blk + 2 * i2));
       gidx[i2 * nblk_s + blk] = pr.x | (pr.y << 16);
     }
     ptx::named_bar_sync(15, cn);
@@ -433,7 +435,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   if constexpr (NORM) {   // gamma in reordered channel order
     const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
     for (int j = ct; j < K; j += cn) {
-      const int pj = use_tab ? perm_s[j] : __ldg(a.perm + j);
+      const int pj = d.perm_smem == 1 ? perm_s[j] : __ldg(a.perm + j);
       gamma_r[j] = __ldg(a.gamma + pj);
     }
     ptx::named_bar_sync(15, cn);
@@ -610,9 +612,13 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   d.nbox = (a.K + 255) / 256;
   const size_t stage_bytes = (size_t)d.nbox * 512 * R;
   // Stage the permutation in smem (gather table) when that still leaves >= 3 stages.
-  const size_t tab_need = (size_t)a.K * 4 + (size_t)16 * (a.K / 32 + 1) * 4;   // perm copy + gather table
-  d.perm_smem = (200 * 1024 - tab_need) / stage_bytes >= 3 ? 1 : 0;
-  const size_t tab_bytes = d.perm_smem ? tab_need : 0;
+  // Gather table in smem: with an asynchronous copy of the permutation when that still
+  // leaves >= 3 stages (mode 1), else built straight from global memory (mode 2: large K,
+  // where the one-time prologue is amortised over many tiles), else none (L1 reads).
+  const size_t gtab = (size_t)16 * (a.K / 32 + 1) * 4;
+  const size_t tab_need = (size_t)a.K * 4 + gtab;
+  d.perm_smem = (200 * 1024 - tab_need) / stage_bytes >= 3 ? 1 : ((200 * 1024 - gtab) / stage_bytes >= 2 ? 2 : 0);
+  const size_t tab_bytes = d.perm_smem == 1 ? tab_need : (d.perm_smem == 2 ? gtab : 0);
   const size_t norm_need = a.gamma ? ((size_t)a.K * 2 + 255) / 256 * 256 + 4096 : 0;
   int stages = (int)((200 * 1024 - tab_bytes - norm_need) / stage_bytes);
   if (stages > 8) stages = 8;
