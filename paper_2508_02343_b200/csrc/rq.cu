@@ -301,6 +301,80 @@ __device__ __forceinline__ void quantize_tile_block(const typename Slot<R>::T (&
   }
 }
 
+// Per-tile context of a consumer warp (everything seg_chunks needs besides the plan).
+template <int R> struct ChunkCtx {
+  const uint8_t* st;        // stage: 256-channel boxes of row-interleaved slots
+  const uint32_t* gidx;     // gather table (byte offsets of slots, two per word) or null
+  int nblk_s;
+  const uint16_t* gamma_r;  // RMSNorm weight in reordered order (NORM only)
+  int64_t r0;               // first row of the tile
+  int nvalid;               // rows of the tile inside the matrix
+  int group_warps, lane, dbg;
+  bool use_tab;
+};
+
+// The chunks of segment G owned by this warp (local chunk c_first, c_first +
+// group_warps, ...) for one tile: gather, (norm), block amax, E8M0 scale, encode,
+// store.  G is a compile-time constant, so the segment's geometry is read straight
+// from the kernel parameters (uniform registers, no per-chunk selects).
+template <int R, bool NORM, int G, int FMT>
+__device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& cx, int c_first, const float (&rn)[4]) {
+  using ST = typename Slot<R>::T;
+  const int kp = a.geom.kp[G], nb = kp / 32, nch = (nb + 15) / 16;
+  if (c_first >= nch) return;
+  const int n = a.geom.n[G], segoff = a.geom.off[G], sco = a.geom.sc_off[G];
+  const int64_t pitch = a.geom.pitch[G];
+  const int h = cx.lane & 1;                       // which half of the block
+  constexpr int hb = G == 0 ? 8 : (G == 1 ? 12 : 16);   // code bytes per half block
+  uint8_t* const crow_base = a.codes[G] + cx.r0 * pitch + h * hb;
+  uint8_t* const sf_base = a.sf[G] + (cx.r0 >> 7) * (int64_t)(kp / 128) * 512 + (cx.r0 & 31) * 16 + ((cx.r0 >> 5) & 3) * 4;
+  for (int c = c_first; c < nch; c += cx.group_warps) {
+    const int kb = c * 16 + (cx.lane >> 1);
+    if (kb >= nb) continue;                        // pair-uniform
+    uint8_t* crow0 = crow_base + kb * (2 * hb);
+    uint8_t* sfp = sf_base + (kb >> 2) * 512 + (kb & 3);
+    if (kb * 32 >= n || (cx.dbg & 8)) {            // padding block: zero codes and zero scale bytes
+      if (cx.dbg & 16) continue;                   // timing experiment: no stores at all
+#pragma unroll
+      for (int rho = 0; rho < R; ++rho) {
+        if (h == 0) sfp[16 * rho] = 0;
+        if (rho < cx.nvalid)
+          for (int b = 0; b < hb; b += 4) *reinterpret_cast<uint32_t*>(crow0 + rho * pitch + b) = 0u;
+      }
+      continue;
+    }
+    ST v[16];
+    if (cx.use_tab) {
+      const uint32_t* gp = cx.gidx + (segoff / 32 + kb) + 8 * h * cx.nblk_s;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t pr = gp[q * cx.nblk_s];
+        v[2 * q + 0] = *reinterpret_cast<const ST*>(cx.st + (pr & 0xFFFFu));
+        v[2 * q + 1] = *reinterpret_cast<const ST*>(cx.st + (pr >> 16));
+      }
+    } else {
+      const ST* slots = reinterpret_cast<const ST*>(cx.st);
+      const int4* pp = reinterpret_cast<const int4*>(a.perm + segoff + 32 * kb + 16 * h);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int4 pv = __ldg(pp + q);
+        v[4 * q + 0] = slots[pv.x];
+        v[4 * q + 1] = slots[pv.y];
+        v[4 * q + 2] = slots[pv.z];
+        v[4 * q + 3] = slots[pv.w];
+      }
+    }
+    if constexpr (NORM) {
+      const uint4* gp4 = reinterpret_cast<const uint4*>(cx.gamma_r + segoff + 32 * kb + 16 * h);
+      const uint4 ga = gp4[0], gb = gp4[1];
+      const uint32_t gw8[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) norm_slot<R>(v[i], (gw8[i >> 1] >> (16 * (i & 1))) & 0xFFFFu, rn);
+    }
+    quantize_tile_block<R, G, FMT, 16>(v, sco, crow0, pitch, sfp, cx.nvalid, h == 0);
+  }
+}
+
 // Timeline trace (env MM_RQ_DEBUG & 32; read with mm_debug_rq_trace): per CTA
 // [start, table ready, tile0 data ready, tile0 done, tile1 ready, tile1 done, ..., last TMA issued].
 __device__ unsigned long long g_rq_trace[160][16];
@@ -328,8 +402,14 @@ struct RqDev {
 //    channel that returns all R rows (the permutation is read through L1 as
 //    16-byte vectors), block amax, scale and encode as above; finally the stage
 //    is released to the producer.
+#ifndef RQ_T2
+#define RQ_T2 768
+#endif
+// Thread budget per variant (register file / threads = registers per lane).
+constexpr int rq_max_threads(int R, bool NORM) { return (R == 4 || NORM) ? 704 : (R == 2 ? RQ_T2 : 1024); }
+
 template <int R, bool NORM>
-__global__ void __launch_bounds__((R == 4 || NORM) ? 704 : 1024, 1)
+__global__ void __launch_bounds__(rq_max_threads(R, NORM), 1)
 rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev d) {
   using ST = typename Slot<R>::T;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -404,19 +484,9 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   // parameter block inside the loop would go through generic/local memory.
   const int stages = d.stages, groups = d.groups, group_warps = d.group_warps, nbox = d.nbox, dbg = d.dbg;
   const int64_t rows = a.rows;
-  const int kp0 = a.geom.kp[0], kp1 = a.geom.kp[1], kp2 = a.geom.kp[2];
-  const int n0 = a.geom.n[0], n1 = a.geom.n[1], n2 = a.geom.n[2];
-  const int of0 = a.geom.off[0], of1 = a.geom.off[1], of2 = a.geom.off[2];
+  const int kp0 = a.geom.kp[0], kp1 = a.geom.kp[1];
   const int fm1 = a.geom.fmt[1], fm2 = a.geom.fmt[2];
-  const int so0 = a.geom.sc_off[0], so1 = a.geom.sc_off[1], so2 = a.geom.sc_off[2];
-  const int64_t pt0 = a.geom.pitch[0], pt1 = a.geom.pitch[1], pt2 = a.geom.pitch[2];
-  uint8_t* const cd0 = a.codes[0];
-  uint8_t* const cd1 = a.codes[1];
-  uint8_t* const cd2 = a.codes[2];
-  uint8_t* const sf0 = a.sf[0];
-  uint8_t* const sf1 = a.sf[1];
-  uint8_t* const sf2 = a.sf[2];
-  // Gather table: u16 channel indices, two per word, transposed [i/2][block] so
+  // Gather table: u16 slot byte offsets, two per word, transposed [i/2][block] so
   // the lanes of a warp (consecutive blocks) read consecutive words.
   const bool use_tab = d.perm_smem != 0;
   if (use_tab) {
@@ -426,7 +496,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       const int blk = t >> 4, i2 = t & 15;
       const uint2 pr = d.perm_smem == 1 ? *reinterpret_cast<const uint2*>(perm_s + 32 * blk + 2 * i2)
                                         : __ldg(reinterpret_cast<const uint2*>(a.perm + 32 * blk + 2 * i2));
-      gidx[i2 * nblk_s + blk] = pr.x | (pr.y << 16);
+      gidx[i2 * nblk_s + blk] = (pr.x * (uint32_t)sizeof(ST)) | ((pr.y * (uint32_t)sizeof(ST)) << 16);
     }
     ptx::named_bar_sync(15, cn);
     if ((d.dbg & 32) && threadIdx.x == 32) g_rq_trace[blockIdx.x][1] = ptx::globaltimer_ns();
@@ -443,12 +513,17 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   const double eps = a.eps;
   // Work is split into chunks of 16 consecutive blocks of ONE segment (a warp's
   // lanes never mix segments, so the encode path is warp-uniform); the two lanes of
-  // a pair share a block, 16 channels each.
-  const int nch0 = (kp0 / 32 + 15) / 16, nch1 = (kp1 / 32 + 15) / 16, nch2 = (kp2 / 32 + 15) / 16;
-  const int nch = nch0 + nch1 + nch2;
+  // a pair share a block, 16 channels each.  Warp gw of a group owns the chunks
+  // ch = gw (mod group_warps) of the concatenated chunk list of the three segments
+  // -- the same chunks in every tile, so their first local index per segment is
+  // fixed per warp.
+  const int nch0 = (kp0 / 32 + 15) / 16, nch1 = (kp1 / 32 + 15) / 16;
+  const int cf0 = gw, cf1 = ((gw - nch0) % group_warps + group_warps) % group_warps,
+            cf2 = ((gw - nch0 - nch1) % group_warps + group_warps) % group_warps;
+  const bool e3m2 = fm1 == F_E3M2, e4m3 = fm2 == F_E4M3;
+  int s = grp;           // ring slot and phase of tile i, advanced incrementally
+  uint32_t ph = 0;       // (groups < stages: at most one wrap per step)
   for (int64_t i = grp; i < my_tiles; i += groups) {
-    const int s = int(i % stages);
-    const uint32_t ph = uint32_t(i / stages) & 1u;
     uint8_t* st = smem + (size_t)s * stage_bytes;
     ptx::mbar_wait(ptx::smem_u32(&full[s]), ph, 12, s, (int)i);
     if ((d.dbg & 32) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][2 + 2 * i] = ptx::globaltimer_ns();
@@ -481,115 +556,63 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       ptx::named_bar_sync(1 + grp, gthreads);
     }
     // ---- gather + quantize + pack + store ----
-    if (dbg & 3) { __syncwarp(); if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s])); continue; }
-    const ST* slots = reinterpret_cast<const ST*>(st);
-    float rn[4] = {0.f, 0.f, 0.f, 0.f};
-    if constexpr (NORM) {
-      // exact per-row sums of squares (double-double), group reduction in a fixed order
-      double hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
-      for (int pc = gw * 32 + lane; pc < K; pc += gthreads) {
-        const ST v = slots[pc];
-        { const double x = bf16_f64(slot_bits<0>(v)); dd_add(hi[0], lo[0], x * x); }
-        if constexpr (R >= 2) { const double x = bf16_f64(slot_bits<1>(v)); dd_add(hi[1], lo[1], x * x); }
-        if constexpr (R >= 4) {
-          { const double x = bf16_f64(slot_bits<2>(v)); dd_add(hi[2], lo[2], x * x); }
-          { const double x = bf16_f64(slot_bits<3>(v)); dd_add(hi[3], lo[3], x * x); }
-        }
-      }
-#pragma unroll
-      for (int rho = 0; rho < R; ++rho)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double oh = __shfl_xor_sync(0xffffffffu, hi[rho], o), ol = __shfl_xor_sync(0xffffffffu, lo[rho], o);
-          dd_add_dd(hi[rho], lo[rho], oh, ol);
-        }
-      // scratch: [consumer warp (<= 31)][rho][hi, lo] doubles, then [group][rho] norms
-      double* red = nred + (grp * group_warps) * 8;
-      if (lane == 0)
-#pragma unroll
-        for (int rho = 0; rho < R; ++rho) { red[gw * 8 + 2 * rho] = hi[rho]; red[gw * 8 + 2 * rho + 1] = lo[rho]; }
-      ptx::named_bar_sync(1 + grp, gthreads);
-      if (gw == 0 && lane < R) {
-        double h2 = 0.0, l2 = 0.0;
-        for (int ww = 0; ww < group_warps; ++ww) dd_add_dd(h2, l2, red[ww * 8 + 2 * lane], red[ww * 8 + 2 * lane + 1]);
-        const double ss = h2 + l2;
-        nred[32 * 8 + grp * 4 + lane] = (double)(float)(1.0 / sqrt(ss / (double)K + eps));   // fp32 row scale
-      }
-      ptx::named_bar_sync(1 + grp, gthreads);
-#pragma unroll
-      for (int rho = 0; rho < R; ++rho) rn[rho] = (float)nred[32 * 8 + grp * 4 + rho];
-    }
-    const int64_t r0 = (blockIdx.x + i * gridDim.x) * (int64_t)R;
-    const int64_t left = rows - r0;
-    const int nvalid = left >= R ? R : (left > 0 ? (int)left : 0);
-    const int h = lane & 1;                      // which half of the block
-    for (int ch = gw; ch < nch; ch += group_warps) {
-      const int g = ch < nch0 ? 0 : (ch < nch0 + nch1 ? 1 : 2);
-      const int kb = (ch - (g == 0 ? 0 : (g == 1 ? nch0 : nch0 + nch1))) * 16 + (lane >> 1);
-      const int kp_g = g == 0 ? kp0 : (g == 1 ? kp1 : kp2);
-      if (kb >= kp_g / 32) continue;             // pair-uniform
-      const int n_g = g == 0 ? n0 : (g == 1 ? n1 : n2);
-      const int off_g = g == 0 ? of0 : (g == 1 ? of1 : of2);
-      const int fmt = g == 1 ? fm1 : fm2;
-      const int off = g == 0 ? so0 : (g == 1 ? so1 : so2);
-      const int64_t pitch = g == 0 ? pt0 : (g == 1 ? pt1 : pt2);
-      uint8_t* sf_g = g == 0 ? sf0 : (g == 1 ? sf1 : sf2);
-      uint8_t* codes_g = g == 0 ? cd0 : (g == 1 ? cd1 : cd2);
-      uint8_t* sfp = sf_g + sf_offset(r0, kb, kp_g / 128);
-      const int hb = g == 0 ? 8 : (g == 1 ? 12 : 16);   // code bytes per half block
-      uint8_t* crow0 = codes_g + r0 * pitch + (int64_t)kb * 2 * hb + h * hb;
-      if (kb * 32 >= n_g || (dbg & 8)) {   // dbg 8: timing experiment, stores only
-        // padding block: zero codes and zero scale bytes
-        if (dbg & 16) continue;             // timing experiment: no stores at all
-#pragma unroll
-        for (int rho = 0; rho < R; ++rho) {
-          if (h == 0) sfp[16 * rho] = 0;
-          if (rho < nvalid)
-            for (int b = 0; b < hb; b += 4) *reinterpret_cast<uint32_t*>(crow0 + rho * pitch + b) = 0u;
-        }
-        continue;
-      }
-      ST v[16];
-      if (use_tab) {
-        const uint32_t* gp = gidx + (off_g / 32 + kb) + 8 * h * nblk_s;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const uint32_t pr = gp[q * nblk_s];
-          v[2 * q + 0] = slots[pr & 0xFFFFu];
-          v[2 * q + 1] = slots[pr >> 16];
-        }
-      } else {
-        const int4* pp = reinterpret_cast<const int4*>(a.perm + off_g + 32 * kb + 16 * h);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int4 pv = __ldg(pp + q);
-          v[4 * q + 0] = slots[pv.x];
-          v[4 * q + 1] = slots[pv.y];
-          v[4 * q + 2] = slots[pv.z];
-          v[4 * q + 3] = slots[pv.w];
-        }
-      }
+    if (dbg & 3) {
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s]));
+    } else {
+      float rn[4] = {0.f, 0.f, 0.f, 0.f};
       if constexpr (NORM) {
-        const uint4* gp4 = reinterpret_cast<const uint4*>(gamma_r + off_g + 32 * kb + 16 * h);
-        const uint4 ga = gp4[0], gb = gp4[1];
-        const uint32_t gw8[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const ST* slots = reinterpret_cast<const ST*>(st);
+        // exact per-row sums of squares (double-double), group reduction in a fixed order
+        double hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+        for (int pc = gw * 32 + lane; pc < K; pc += gthreads) {
+          const ST v = slots[pc];
+          { const double x = bf16_f64(slot_bits<0>(v)); dd_add(hi[0], lo[0], x * x); }
+          if constexpr (R >= 2) { const double x = bf16_f64(slot_bits<1>(v)); dd_add(hi[1], lo[1], x * x); }
+          if constexpr (R >= 4) {
+            { const double x = bf16_f64(slot_bits<2>(v)); dd_add(hi[2], lo[2], x * x); }
+            { const double x = bf16_f64(slot_bits<3>(v)); dd_add(hi[3], lo[3], x * x); }
+          }
+        }
 #pragma unroll
-        for (int i = 0; i < 16; ++i) norm_slot<R>(v[i], (gw8[i >> 1] >> (16 * (i & 1))) & 0xFFFFu, rn);
+        for (int rho = 0; rho < R; ++rho)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double oh = __shfl_xor_sync(0xffffffffu, hi[rho], o), ol = __shfl_xor_sync(0xffffffffu, lo[rho], o);
+            dd_add_dd(hi[rho], lo[rho], oh, ol);
+          }
+        // scratch: [consumer warp (<= 31)][rho][hi, lo] doubles, then [group][rho] norms
+        double* red = nred + (grp * group_warps) * 8;
+        if (lane == 0)
+#pragma unroll
+          for (int rho = 0; rho < R; ++rho) { red[gw * 8 + 2 * rho] = hi[rho]; red[gw * 8 + 2 * rho + 1] = lo[rho]; }
+        ptx::named_bar_sync(1 + grp, gthreads);
+        if (gw == 0 && lane < R) {
+          double h2 = 0.0, l2 = 0.0;
+          for (int ww = 0; ww < group_warps; ++ww) dd_add_dd(h2, l2, red[ww * 8 + 2 * lane], red[ww * 8 + 2 * lane + 1]);
+          const double ss = h2 + l2;
+          nred[32 * 8 + grp * 4 + lane] = (double)(float)(1.0 / sqrt(ss / (double)K + eps));   // fp32 row scale
+        }
+        ptx::named_bar_sync(1 + grp, gthreads);
+#pragma unroll
+        for (int rho = 0; rho < R; ++rho) rn[rho] = (float)nred[32 * 8 + grp * 4 + rho];
       }
-      const bool sf_lane = h == 0;
-      if (g == 0) quantize_tile_block<R, 0, F_E2M1, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
-      else if (g == 1) {
-        if (fmt == F_E3M2) quantize_tile_block<R, 1, F_E3M2, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
-        else quantize_tile_block<R, 1, F_E2M3, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
-      } else {
-        if (fmt == F_E4M3) quantize_tile_block<R, 2, F_E4M3, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
-        else quantize_tile_block<R, 2, F_E5M2, 16>(v, off, crow0, pitch, sfp, nvalid, sf_lane);
-      }
+      const int64_t r0 = (blockIdx.x + i * gridDim.x) * (int64_t)R;
+      const int64_t left = rows - r0;
+      const int nvalid = left >= R ? R : (left > 0 ? (int)left : 0);
+      const ChunkCtx<R> cx{st, gidx, nblk_s, gamma_r, r0, nvalid, group_warps, lane, dbg, use_tab};
+      seg_chunks<R, NORM, 0, F_E2M1>(a, cx, cf0, rn);
+      if (e3m2) seg_chunks<R, NORM, 1, F_E3M2>(a, cx, cf1, rn);
+      else seg_chunks<R, NORM, 1, F_E2M3>(a, cx, cf1, rn);
+      if (e4m3) seg_chunks<R, NORM, 2, F_E4M3>(a, cx, cf2, rn);
+      else seg_chunks<R, NORM, 2, F_E5M2>(a, cx, cf2, rn);
+      if ((d.dbg & 32) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][3 + 2 * i] = ptx::globaltimer_ns();
+      // ---- release the stage (every warp of the group arrives once) ----
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s]));
     }
-    if ((d.dbg & 32) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][3 + 2 * i] = ptx::globaltimer_ns();
-    // ---- release the stage (every warp of the group arrives once) ----
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s]));
+    s += groups;
+    if (s >= stages) { s -= stages; ph ^= 1u; }
   }
 }
 
@@ -618,6 +641,7 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   const size_t gtab = (size_t)16 * (a.K / 32 + 1) * 4;
   const size_t tab_need = (size_t)a.K * 4 + gtab;
   d.perm_smem = (200 * 1024 - tab_need) / stage_bytes >= 3 ? 1 : ((200 * 1024 - gtab) / stage_bytes >= 2 ? 2 : 0);
+  if ((size_t)a.K * 2 * R > 65536) d.perm_smem = 0;   // table holds u16 slot byte offsets
   const size_t tab_bytes = d.perm_smem == 1 ? tab_need : (d.perm_smem == 2 ? gtab : 0);
   const size_t norm_need = a.gamma ? ((size_t)a.K * 2 + 255) / 256 * 256 + 4096 : 0;
   int stages = (int)((200 * 1024 - tab_bytes - norm_need) / stage_bytes);
@@ -629,7 +653,7 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   if (gw > 12) gw = 12;
   if (gw < 2) gw = 2;
   d.group_warps = gw;
-  int groups = ((R == 4 || NORM) ? 21 : 31) / gw;   // consumer warps (+ the producer warp) within the register budget
+  int groups = (rq_max_threads(R, NORM) / 32 - 1) / gw;   // consumer warps (+ the producer warp) within the register budget
   if (groups > stages - 1) groups = stages - 1;
   if (groups < 1) groups = 1;
   d.groups = groups;

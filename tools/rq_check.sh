@@ -1,3 +1,3 @@
-timeout 300 python -m pytest tests/test_gpu_rq.py tests/test_gpu_gemm.py -q -p no:cacheprovider -o timeout=120 2>&1 | tail -3
-timeout 200 python bench.py --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); b=d['breakdown']; print('step_us', round(d['ms_per_step']*1e3,1), 'gemm_us', round(b['gemm_us'],1), 'rq_us', round(b['rq_us'],2), 'rq_GBs', round(b['rq_gbs']), 'frac', round(b['rq_frac_hbm'],3), 'e2e', round(d['e2e']['value']))"
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none -k regex:"rq_kernel" -s 14 -c 2 --csv python bench.py --no-cpu-baseline --steps 3 2>/dev/null | grep -E "rq_kernel" | awk -F'","' '{print $5, $(NF-2), $NF}' | cut -c1-200
+# RQ change check: GPU RQ tests + the RQ columns of the config sweep (C2, C3, C4)
+timeout 300 python -m pytest tests/test_gpu_rq.py tests/test_gpu_gemm.py -q -p no:cacheprovider -o timeout=120 2>&1 | tail -2
+timeout 1200 python tools/sweep_configs.py rqcheck c2,c3,c4 2>&1 | grep "^| C" | cut -d'|' -f2,6,7,8
