@@ -22,6 +22,10 @@ struct SegGeom {
   int64_t pitch[3];  // code bytes per row
 };
 
+// Dynamic shared memory the reorder-quantize kernel may use for its ring, gather
+// table and norm scratch (the 227 KB opt-in limit minus alignment and barriers).
+constexpr size_t kRqSmemBudget = 227 * 1024 - 2048;
+
 struct RqArgs {
   const uint16_t* x;   // BF16 bits [rows, ldx]
   int64_t rows;

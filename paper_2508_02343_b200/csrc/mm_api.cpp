@@ -147,7 +147,7 @@ uint64_t fingerprint(int32_t K, const int32_t n[3], int32_t fmt6, int32_t fmt8, 
 }
 
 // Shared memory the reorder-quantize kernel needs for this K (R = 1 layout).
-bool rq_fits(int32_t K) { return (size_t)((K + 255) / 256) * 512 * 2 <= 200 * 1024; }   // >= 2 one-row stages
+bool rq_fits(int32_t K) { return (size_t)((K + 255) / 256) * 512 * 2 <= kRqSmemBudget; }   // >= 2 one-row stages
 
 mm_status check_mx_out(const mm_plan* p, const mm_mx_tensor* t, int64_t rows, const char* what) {
   if (!t) return fail(MM_ERR_INVALID_ARGUMENT, "%s is NULL", what);

@@ -51,6 +51,32 @@ static __device__ __noinline__ void watchdog_fire(int tag, uint32_t bar, uint32_
          blockIdx.x, threadIdx.x, tag, bar, parity, a, b);
   __trap();
 }
+// try_wait with a suspend-time hint (ns): the waiting thread sleeps until the phase
+// completes or the hint expires, instead of re-polling (for warps that wait long).
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, int tag = 0, int a = 0, int b = 0) {
+#if MM_WATCHDOG_NS
+  uint64_t t0 = 0;
+  for (uint32_t n = 0; !mbar_try_wait_hint(bar, parity, 20000u); ++n) {
+    if (n == 0) t0 = globaltimer_ns();
+    else if (globaltimer_ns() - t0 > (uint64_t)MM_WATCHDOG_NS) watchdog_fire(tag, bar, parity, a, b);
+  }
+#else
+  while (!mbar_try_wait_hint(bar, parity, 20000u)) {
+  }
+#endif
+}
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag = 0, int a = 0, int b = 0) {
   if (mbar_try_wait(bar, parity)) return;
 #if MM_WATCHDOG_NS

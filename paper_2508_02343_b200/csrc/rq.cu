@@ -27,6 +27,12 @@
 #include "internal.h"
 #include "ptx.cuh"
 
+// Timing experiments and the timeline trace (env MM_RQ_DEBUG) are compiled in only
+// with -DMM_RQ_EXPERIMENTS=1; the product build folds every check away.
+#ifndef MM_RQ_EXPERIMENTS
+#define MM_RQ_EXPERIMENTS 0
+#endif
+
 namespace mmx {
 namespace {
 
@@ -247,31 +253,48 @@ __device__ __forceinline__ void block_amax(const uint16_t (&v)[NV], uint32_t (&a
   if constexpr (NV == 16) m = max(m, __shfl_xor_sync(3u << (threadIdx.x & 30), m, 1));
   am[0] = m;
 }
+// max(|a|, |b|) per BF16 half (sign = xor of the signs; masked off by the caller):
+// one instruction per word instead of an abs-mask and an integer max.  Inputs are
+// finite (NaN/Inf are outside the contract, R8); subnormals are ordered
+// exactly like their bit patterns.
+__device__ __forceinline__ uint32_t absmax_bf16x2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// Pairwise tree over NV (a power of two) words: log2(NV) dependent steps, not NV.
+template <int NV, typename F>
+__device__ __forceinline__ uint32_t tree_reduce(const uint32_t (&w)[NV], F f) {
+  uint32_t t[NV / 2];
+#pragma unroll
+  for (int i = 0; i < NV / 2; ++i) t[i] = f(w[2 * i], w[2 * i + 1]);
+#pragma unroll
+  for (int n = NV / 4; n >= 1; n /= 2)
+#pragma unroll
+    for (int i = 0; i < n; ++i) t[i] = f(t[2 * i], t[2 * i + 1]);
+  return t[0];
+}
 template <int NV>
 __device__ __forceinline__ void block_amax(const uint32_t (&v)[NV], uint32_t (&am)[4]) {
-  uint32_t m = 0;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) m = __vmaxu2(m, v[i] & 0x7FFF7FFFu);
-  if constexpr (NV == 16) m = __vmaxu2(m, __shfl_xor_sync(3u << (threadIdx.x & 30), m, 1));
-  am[0] = m & 0xFFFFu;
-  am[1] = m >> 16;
+  uint32_t m = tree_reduce<NV>(v, absmax_bf16x2);
+  if constexpr (NV == 16) m = absmax_bf16x2(m, __shfl_xor_sync(3u << (threadIdx.x & 30), m, 1));
+  am[0] = m & 0x7FFFu;
+  am[1] = (m >> 16) & 0x7FFFu;
 }
 template <int NV>
 __device__ __forceinline__ void block_amax(const uint2 (&v)[NV], uint32_t (&am)[4]) {
-  uint32_t m01 = 0, m23 = 0;
+  uint32_t x[NV], y[NV];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    m01 = __vmaxu2(m01, v[i].x & 0x7FFF7FFFu);
-    m23 = __vmaxu2(m23, v[i].y & 0x7FFF7FFFu);
-  }
+  for (int i = 0; i < NV; ++i) { x[i] = v[i].x; y[i] = v[i].y; }
+  uint32_t m01 = tree_reduce<NV>(x, absmax_bf16x2), m23 = tree_reduce<NV>(y, absmax_bf16x2);
   if constexpr (NV == 16) {
-    m01 = __vmaxu2(m01, __shfl_xor_sync(3u << (threadIdx.x & 30), m01, 1));
-    m23 = __vmaxu2(m23, __shfl_xor_sync(3u << (threadIdx.x & 30), m23, 1));
+    m01 = absmax_bf16x2(m01, __shfl_xor_sync(3u << (threadIdx.x & 30), m01, 1));
+    m23 = absmax_bf16x2(m23, __shfl_xor_sync(3u << (threadIdx.x & 30), m23, 1));
   }
-  am[0] = m01 & 0xFFFFu;
-  am[1] = m01 >> 16;
-  am[2] = m23 & 0xFFFFu;
-  am[3] = m23 >> 16;
+  am[0] = m01 & 0x7FFFu;
+  am[1] = (m01 >> 16) & 0x7FFFu;
+  am[2] = m23 & 0x7FFFu;
+  am[3] = (m23 >> 16) & 0x7FFFu;
 }
 
 // One row of one block: E8M0 exponent by integer arithmetic on the BF16 exponent
@@ -305,9 +328,8 @@ __device__ __forceinline__ void quantize_tile_block(const typename Slot<R>::T (&
 template <int R> struct ChunkCtx {
   const uint8_t* st;        // stage: 256-channel boxes of row-interleaved slots
   const uint32_t* gidx;     // gather table (byte offsets of slots, two per word) or null
-  int nblk_s;
   const uint16_t* gamma_r;  // RMSNorm weight in reordered order (NORM only)
-  int64_t r0;               // first row of the tile
+  int r0;                   // first row of the tile
   int nvalid;               // rows of the tile inside the matrix
   int group_warps, lane, dbg;
   bool use_tab;
@@ -320,19 +342,20 @@ template <int R> struct ChunkCtx {
 template <int R, bool NORM, int G, int FMT>
 __device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& cx, int c_first, const float (&rn)[4]) {
   using ST = typename Slot<R>::T;
-  const int kp = a.geom.kp[G], nb = kp / 32, nch = (nb + 15) / 16;
+  const int kp = a.geom.kp[G], nb = (unsigned)kp >> 5, nch = (unsigned)(nb + 15) >> 4;
   if (c_first >= nch) return;
   const int n = a.geom.n[G], segoff = a.geom.off[G], sco = a.geom.sc_off[G];
   const int64_t pitch = a.geom.pitch[G];
   const int h = cx.lane & 1;                       // which half of the block
   constexpr int hb = G == 0 ? 8 : (G == 1 ? 12 : 16);   // code bytes per half block
-  uint8_t* const crow_base = a.codes[G] + cx.r0 * pitch + h * hb;
-  uint8_t* const sf_base = a.sf[G] + (cx.r0 >> 7) * (int64_t)(kp / 128) * 512 + (cx.r0 & 31) * 16 + ((cx.r0 >> 5) & 3) * 4;
+  const unsigned r0 = (unsigned)cx.r0;
+  uint8_t* const crow_base = a.codes[G] + (int64_t)r0 * pitch + h * hb;
+  uint8_t* const sf_base = a.sf[G] + (size_t)((r0 >> 7) * ((unsigned)kp >> 7)) * 512 + (r0 & 31) * 16 + ((r0 >> 5) & 3) * 4;
   for (int c = c_first; c < nch; c += cx.group_warps) {
     const int kb = c * 16 + (cx.lane >> 1);
     if (kb >= nb) continue;                        // pair-uniform
-    uint8_t* crow0 = crow_base + kb * (2 * hb);
-    uint8_t* sfp = sf_base + (kb >> 2) * 512 + (kb & 3);
+    uint8_t* crow0 = crow_base + (unsigned)kb * (2 * hb);
+    uint8_t* sfp = sf_base + ((unsigned)kb >> 2) * 512 + (kb & 3);
     if (kb * 32 >= n || (cx.dbg & 8)) {            // padding block: zero codes and zero scale bytes
       if (cx.dbg & 16) continue;                   // timing experiment: no stores at all
 #pragma unroll
@@ -345,12 +368,13 @@ __device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& c
     }
     ST v[16];
     if (cx.use_tab) {
-      const uint32_t* gp = cx.gidx + (segoff / 32 + kb) + 8 * h * cx.nblk_s;
+      const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + 16 * ((segoff >> 5) + kb) + 8 * h);
+      const uint4 p0 = gp[0], p1 = gp[1];
+      const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const uint32_t pr = gp[q * cx.nblk_s];
-        v[2 * q + 0] = *reinterpret_cast<const ST*>(cx.st + (pr & 0xFFFFu));
-        v[2 * q + 1] = *reinterpret_cast<const ST*>(cx.st + (pr >> 16));
+        v[2 * q + 0] = *reinterpret_cast<const ST*>(cx.st + (pr[q] & 0xFFFFu));
+        v[2 * q + 1] = *reinterpret_cast<const ST*>(cx.st + (pr[q] >> 16));
       }
     } else {
       const ST* slots = reinterpret_cast<const ST*>(cx.st);
@@ -402,11 +426,14 @@ struct RqDev {
 //    channel that returns all R rows (the permutation is read through L1 as
 //    16-byte vectors), block amax, scale and encode as above; finally the stage
 //    is released to the producer.
+#ifndef RQ_T4
+#define RQ_T4 640
+#endif
 #ifndef RQ_T2
 #define RQ_T2 768
 #endif
 // Thread budget per variant (register file / threads = registers per lane).
-constexpr int rq_max_threads(int R, bool NORM) { return (R == 4 || NORM) ? 704 : (R == 2 ? RQ_T2 : 1024); }
+constexpr int rq_max_threads(int R, bool NORM) { return (R == 4 || NORM) ? RQ_T4 : (R == 2 ? RQ_T2 : 1024); }
 
 template <int R, bool NORM>
 __global__ void __launch_bounds__(rq_max_threads(R, NORM), 1)
@@ -419,11 +446,11 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   const RqArgs& a = d.a;
   const int stage_bytes = d.nbox * 512 * R;
   // [ring of stages][perm copy: K x int32][gather table: K x u16][barriers]
-  const int K = a.K, nblk = K / 32, nblk_s = nblk + 1;   // table row stride padded (bank spread)
+  const int K = a.K;
   const size_t perm_copy = d.perm_smem == 1 ? (size_t)K * 4 : 0;
-  const size_t tab_bytes = d.perm_smem ? perm_copy + (size_t)16 * (K / 32 + 1) * 4 : 0;
+  const size_t tab_bytes = d.perm_smem ? perm_copy + ((size_t)K * 2 + 15) / 16 * 16 : 0;
   const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
-  uint32_t* gidx = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + perm_copy);   // 16 x nblk_s words
+  uint32_t* gidx = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + perm_copy);   // K/2 words
   // optional RMSNorm region: gamma in reordered order (K x u16) + reduction scratch
   constexpr bool norm = NORM;   // RMSNorm fused ahead of the quantization (a.gamma != nullptr)
   const size_t norm_bytes = norm ? ((size_t)K * 2 + 255) / 256 * 256 + 4096 : 0;
@@ -435,7 +462,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   uint64_t* permbar = empty + d.stages;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint64_t t_start = ptx::globaltimer_ns();
-  if (threadIdx.x == 0 && (d.dbg & 32)) g_rq_trace[blockIdx.x][0] = t_start;
+  if (threadIdx.x == 0 && (MM_RQ_EXPERIMENTS && (d.dbg & 32))) g_rq_trace[blockIdx.x][0] = t_start;
   if (threadIdx.x == 0) {
     for (int i = 0; i < d.stages; ++i) {
       ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
@@ -461,16 +488,16 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       for (int64_t i = 0; i < my_tiles; ++i) {
         const int s = int(i % d.stages);
         const uint32_t ph = uint32_t(i / d.stages) & 1u;
-        ptx::mbar_wait(ptx::smem_u32(&empty[s]), ph ^ 1u, 11, s, (int)i);
+        ptx::mbar_wait_sleep(ptx::smem_u32(&empty[s]), ph ^ 1u, 11, s, (int)i);
         const uint32_t fb = ptx::smem_u32(&full[s]);
-        if (d.dbg & 4) { ptx::mbar_arrive(fb); continue; }   // timing experiment: no loads
+        if (MM_RQ_EXPERIMENTS && (d.dbg & 4)) { ptx::mbar_arrive(fb); continue; }   // timing experiment: no loads
         ptx::mbar_arrive_expect_tx(fb, tx);
         const int row0 = (int)((blockIdx.x + i * gridDim.x) * R);
         const uint32_t dst = ptx::smem_u32(smem + (size_t)s * stage_bytes);
         if (d.box3d) ptx::tma_load_3d(dst, &tmx, fb, 0, row0, 0);   // all boxes of the tile at once
         else
           for (int b = 0; b < d.nbox; ++b) ptx::tma_load_2d(dst + b * 512 * R, &tmx, fb, 256 * b, row0);
-        if ((d.dbg & 32) && i == my_tiles - 1) g_rq_trace[blockIdx.x][14] = ptx::globaltimer_ns();
+        if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && i == my_tiles - 1) g_rq_trace[blockIdx.x][14] = ptx::globaltimer_ns();
       }
     }
     return;
@@ -482,24 +509,25 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   const int gthreads = d.group_warps * 32;
   // Kernel parameters are copied into (uniform) registers once: indexing the
   // parameter block inside the loop would go through generic/local memory.
-  const int stages = d.stages, groups = d.groups, group_warps = d.group_warps, nbox = d.nbox, dbg = d.dbg;
+  const int stages = d.stages, groups = d.groups, group_warps = d.group_warps, nbox = d.nbox;
+  const int dbg = MM_RQ_EXPERIMENTS ? d.dbg : 0;
   const int64_t rows = a.rows;
   const int kp0 = a.geom.kp[0], kp1 = a.geom.kp[1];
   const int fm1 = a.geom.fmt[1], fm2 = a.geom.fmt[2];
-  // Gather table: u16 slot byte offsets, two per word, transposed [i/2][block] so
-  // the lanes of a warp (consecutive blocks) read consecutive words.
+  // Gather table: u16 slot byte offsets, two per word, [block][16 words]: the lane
+  // holding half h of block b reads words 16 b + 8 h .. + 7 with two 128-bit loads
+  // (the warp reads 1 KB contiguously: conflict free).
   const bool use_tab = d.perm_smem != 0;
   if (use_tab) {
     if (d.perm_smem == 1) ptx::mbar_wait(ptx::smem_u32(permbar), 0, 13, 0, 0);
     const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
     for (int t = ct; t < K / 2; t += cn) {
-      const int blk = t >> 4, i2 = t & 15;
-      const uint2 pr = d.perm_smem == 1 ? *reinterpret_cast<const uint2*>(perm_s + 32 * blk + 2 * i2)
-                                        : __ldg(reinterpret_cast<const uint2*>(a.perm + 32 * blk + 2 * i2));
-      gidx[i2 * nblk_s + blk] = (pr.x * (uint32_t)sizeof(ST)) | ((pr.y * (uint32_t)sizeof(ST)) << 16);
+      const uint2 pr = d.perm_smem == 1 ? *reinterpret_cast<const uint2*>(perm_s + 2 * t)
+                                        : __ldg(reinterpret_cast<const uint2*>(a.perm + 2 * t));
+      gidx[t] = (pr.x * (uint32_t)sizeof(ST)) | ((pr.y * (uint32_t)sizeof(ST)) << 16);
     }
     ptx::named_bar_sync(15, cn);
-    if ((d.dbg & 32) && threadIdx.x == 32) g_rq_trace[blockIdx.x][1] = ptx::globaltimer_ns();
+    if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && threadIdx.x == 32) g_rq_trace[blockIdx.x][1] = ptx::globaltimer_ns();
   }
   ptx::grid_dep_wait();   // the outputs may still be read by the preceding kernel
   if constexpr (NORM) {   // gamma in reordered channel order
@@ -526,7 +554,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   for (int64_t i = grp; i < my_tiles; i += groups) {
     uint8_t* st = smem + (size_t)s * stage_bytes;
     ptx::mbar_wait(ptx::smem_u32(&full[s]), ph, 12, s, (int)i);
-    if ((d.dbg & 32) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][2 + 2 * i] = ptx::globaltimer_ns();
+    if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][2 + 2 * i] = ptx::globaltimer_ns();
     // ---- in-place transpose: box [R rows][256] -> 256 slots of R values ----
     if constexpr (R > 1) {
       for (int b = gw; b < nbox && dbg < 2; b += group_warps) {
@@ -600,13 +628,13 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       const int64_t r0 = (blockIdx.x + i * gridDim.x) * (int64_t)R;
       const int64_t left = rows - r0;
       const int nvalid = left >= R ? R : (left > 0 ? (int)left : 0);
-      const ChunkCtx<R> cx{st, gidx, nblk_s, gamma_r, r0, nvalid, group_warps, lane, dbg, use_tab};
+      const ChunkCtx<R> cx{st, gidx, gamma_r, (int)r0, nvalid, group_warps, lane, dbg, use_tab};
       seg_chunks<R, NORM, 0, F_E2M1>(a, cx, cf0, rn);
       if (e3m2) seg_chunks<R, NORM, 1, F_E3M2>(a, cx, cf1, rn);
       else seg_chunks<R, NORM, 1, F_E2M3>(a, cx, cf1, rn);
       if (e4m3) seg_chunks<R, NORM, 2, F_E4M3>(a, cx, cf2, rn);
       else seg_chunks<R, NORM, 2, F_E5M2>(a, cx, cf2, rn);
-      if ((d.dbg & 32) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][3 + 2 * i] = ptx::globaltimer_ns();
+      if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][3 + 2 * i] = ptx::globaltimer_ns();
       // ---- release the stage (every warp of the group arrives once) ----
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s]));
@@ -638,24 +666,36 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   // Gather table in smem: with an asynchronous copy of the permutation when that still
   // leaves >= 3 stages (mode 1), else built straight from global memory (mode 2: large K,
   // where the one-time prologue is amortised over many tiles), else none (L1 reads).
-  const size_t gtab = (size_t)16 * (a.K / 32 + 1) * 4;
+  const size_t gtab = ((size_t)a.K * 2 + 15) / 16 * 16;
   const size_t tab_need = (size_t)a.K * 4 + gtab;
-  d.perm_smem = (200 * 1024 - tab_need) / stage_bytes >= 3 ? 1 : ((200 * 1024 - gtab) / stage_bytes >= 2 ? 2 : 0);
+  d.perm_smem = (kRqSmemBudget - tab_need) / stage_bytes >= 3 ? 1 : ((kRqSmemBudget - gtab) / stage_bytes >= 2 ? 2 : 0);
   if ((size_t)a.K * 2 * R > 65536) d.perm_smem = 0;   // table holds u16 slot byte offsets
   const size_t tab_bytes = d.perm_smem == 1 ? tab_need : (d.perm_smem == 2 ? gtab : 0);
   const size_t norm_need = a.gamma ? ((size_t)a.K * 2 + 255) / 256 * 256 + 4096 : 0;
-  int stages = (int)((200 * 1024 - tab_bytes - norm_need) / stage_bytes);
-  if (stages > 8) stages = 8;
+  int stages = (int)((kRqSmemBudget - tab_bytes - norm_need) / stage_bytes);
+  if (stages > 32) stages = 32;
   { const char* e = getenv("MM_RQ_STAGES"); if (e && atoi(e) >= 2 && atoi(e) < stages) stages = atoi(e); }
   if (stages < 2) return cudaErrorInvalidConfiguration;
   d.stages = stages;
-  int gw = (a.geom.kp[0] / 32 + 15) / 16 + (a.geom.kp[1] / 32 + 15) / 16 + (a.geom.kp[2] / 32 + 15) / 16;
-  if (gw > 12) gw = 12;
-  if (gw < 2) gw = 2;
-  d.group_warps = gw;
-  int groups = (rq_max_threads(R, NORM) / 32 - 1) / gw;   // consumer warps (+ the producer warp) within the register budget
+  // Consumer layout: W warps (register budget) in `groups` groups of gw warps; a group
+  // works on one tile, warp gw of it on chunks gw, gw + group_warps, ... .  Per-tile
+  // overhead (ring wait, transpose barrier, row bases) is paid per warp, so each warp
+  // should own several chunks (~5 measured best); more groups need more stages.
+  const int nch = (a.geom.kp[0] / 32 + 15) / 16 + (a.geom.kp[1] / 32 + 15) / 16 + (a.geom.kp[2] / 32 + 15) / 16;
+  const int W = rq_max_threads(R, NORM) / 32 - 1;
+  int gw = (nch + 4) / 5;
+  if (gw < 1) gw = 1;
+  if (gw > W) gw = W;
+  int groups = W / gw;
+  if (groups > stages - 1) {   // stage-limited: fewer, larger groups that still use every warp
+    groups = stages - 1;
+    gw = W / groups;
+    if (gw > nch) gw = nch;
+  }
+  { const char* e = getenv("MM_RQ_GW"); if (e && atoi(e) >= 1 && atoi(e) <= W) { gw = atoi(e); groups = W / gw; } }   // tuning
   if (groups > stages - 1) groups = stages - 1;
   if (groups < 1) groups = 1;
+  d.group_warps = gw;
   d.groups = groups;
   { const char* e = getenv("MM_RQ_DEBUG"); d.dbg = e ? atoi(e) : 0; }
   // TMA map over X.  Preferred: a 3-D view {256 channels, rows, K/256 boxes} with
@@ -708,7 +748,7 @@ cudaError_t launch_reorder_quantize(const RqArgs& a, cudaStream_t s, int64_t* la
   // Two-row tiles while >= 3 stages fit (measured faster than four-row tiles at
   // q_proj: twice the tiles balance the persistent grid, fewer registers per lane
   // allow more consumer warps), single rows beyond.
-  if (2 * row_bytes * 3 <= 200 * 1024) return (a.gamma ? launch_rq_t<2, true>(a, s, launches) : launch_rq_t<2, false>(a, s, launches));
+  if (2 * row_bytes * 3 <= kRqSmemBudget && a.K * 4 <= 65536) return (a.gamma ? launch_rq_t<2, true>(a, s, launches) : launch_rq_t<2, false>(a, s, launches));
   return (a.gamma ? launch_rq_t<1, true>(a, s, launches) : launch_rq_t<1, false>(a, s, launches));
 }
 
