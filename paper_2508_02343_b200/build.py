@@ -35,6 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177",
            "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + sources() + ["-ldl"]
+    extra = os.environ.get("MM_NVCC_FLAGS", "").split()   # e.g. -DMM_RQ_EXPERIMENTS=1 (tuning builds)
+    cmd[1:1] = extra
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

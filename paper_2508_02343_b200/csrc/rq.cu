@@ -692,6 +692,15 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
     gw = W / groups;
     if (gw > nch) gw = nch;
   }
+  // Few tiles per CTA (small M): no more groups than tiles, each with more warps, so
+  // every warp has work in the first round and a tile's latency shrinks.
+  const int64_t grid_est = d.n_tiles < (int64_t)sm_count() ? d.n_tiles : (int64_t)sm_count();
+  const int64_t tpc = (d.n_tiles + grid_est - 1) / grid_est;
+  if (groups > tpc) {
+    groups = (int)tpc;
+    gw = W / groups;
+    if (gw > nch) gw = nch;
+  }
   { const char* e = getenv("MM_RQ_GW"); if (e && atoi(e) >= 1 && atoi(e) <= W) { gw = atoi(e); groups = W / gw; } }   // tuning
   if (groups > stages - 1) groups = stages - 1;
   if (groups < 1) groups = 1;
