@@ -75,6 +75,7 @@ struct GemmConfig {
   int num_stages = 0;   // 0 = auto
   int max_ctas = 0;     // 0 = #SMs
   bool no_stream_k = false;  // keep the data-parallel tiling (N-shard path: shard-independent results)
+  int cluster_pairs = 0;     // CTA-pair GEMM: pairs per cluster (1, 2; 0 = default / MM_GEMM_CP)
 };
 
 // Mixed block-scaled GEMM (gemm.cu).
@@ -123,6 +124,27 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = no_pdl ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+// Same, with a thread-block cluster of `cluster` CTAs along x.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
+                               Args&&... args) {
+  static const bool no_pdl = [] { const char* e = getenv("MM_NO_PDL"); return e && atoi(e); }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 1 : 2;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 cudaError_t cached_occupancy(const void* func, int threads, size_t smem, int* per_sm);

@@ -236,6 +236,16 @@ __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const void* desc, 
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(bar & 0xFEFFFFFFu)
       : "memory");
 }
+// Same, multicast: the box lands at `dst` in every CTA of `mask`; each destination's
+// bytes complete on the barrier of that CTA's pair leader (CUTLASS SM100_TMA_2SM_LOAD_MULTICAST).
+__device__ __forceinline__ void tma_load_2d_cg2_mc(uint32_t dst, const void* desc, uint32_t bar, int32_t c0, int32_t c1,
+                                                   uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(bar & 0xFEFFFFFFu), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_cg2(uint32_t dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "r"(ncols)
                : "memory");
@@ -281,7 +291,8 @@ __device__ __forceinline__ void tc_mma_mxf4_cg2(uint32_t d, uint64_t adesc, uint
 // scale-factor ids 0..3) + a commit that frees the smem stage in both CTAs.
 __device__ __forceinline__ void stage_f8f6_cg2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id0, uint32_t sfa,
                                                uint32_t sfb, uint64_t sda, uint64_t sdb0, uint64_t sdb1,
-                                               uint32_t accum, uint32_t empty_bar, uint32_t do_cp = 1) {
+                                               uint32_t accum, uint32_t empty_bar, uint32_t do_cp = 1,
+                                               uint16_t mask = 3) {
   const uint32_t sfb4 = sfb + 4;
   const uint32_t id1 = id0 | (1u << 29) | (1u << 4), id2 = id0 | (2u << 29) | (2u << 4), id3 = id0 | (3u << 29) | (3u << 4);
   asm volatile(
@@ -301,14 +312,14 @@ __device__ __forceinline__ void stage_f8f6_cg2(uint32_t d, uint64_t ad, uint64_t
       "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a3, b3, %12, [%4], [%5], one;\n\t"
       "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%14], %15;\n\t}"
       ::"r"(d), "l"(ad), "l"(bd), "r"(id0), "r"(sfa), "r"(sfb), "l"(sda), "l"(sdb0), "l"(sdb1), "r"(accum),
-        "r"(id1), "r"(id2), "r"(id3), "r"(sfb4), "r"(empty_bar), "h"((uint16_t)3), "r"(do_cp)
+        "r"(id1), "r"(id2), "r"(id3), "r"(sfb4), "r"(empty_bar), "h"(mask), "r"(do_cp)
       : "memory");
 }
 // One full FP4 stage: 2 atoms each of SFA and of SFB row groups 0/1 + 4
 // kind::mxf4 MMAs (K = 64; MMA k uses atom k/2, scale-factor ids 0/2) + commit.
 __device__ __forceinline__ void stage_f4_cg2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id0, uint32_t sfa,
                                              uint32_t sfb, uint64_t sda, uint64_t sdb0, uint64_t sdb1,
-                                             uint32_t accum, uint32_t empty_bar) {
+                                             uint32_t accum, uint32_t empty_bar, uint16_t mask = 3) {
   // SFA atoms at columns sfa, sfa+4; SFB (atom a, row group r) at sfb + (2a + r) * 4
   const uint32_t sfa4 = sfa + 4, sfb4 = sfb + 4, sfb8 = sfb + 8, sfb12 = sfb + 12;
   const uint32_t id2 = id0 | (2u << 29) | (2u << 4);
@@ -332,14 +343,14 @@ __device__ __forceinline__ void stage_f4_cg2(uint32_t d, uint64_t ad, uint64_t b
       "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a3, b3, %10, [%11], [%13], one;\n\t"
       "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%15], %16;\n\t}"
       ::"r"(d), "l"(ad), "l"(bd), "r"(id0), "r"(sfa), "r"(sfb), "l"(sda), "l"(sdb0), "l"(sdb1), "r"(accum),
-        "r"(id2), "r"(sfa4), "r"(sfb4), "r"(sfb8), "r"(sfb12), "r"(empty_bar), "h"((uint16_t)3)
+        "r"(id2), "r"(sfa4), "r"(sfb4), "r"(sfb8), "r"(sfb12), "r"(empty_bar), "h"(mask)
       : "memory");
 }
-__device__ __forceinline__ void commit_cg2_mc_elect(uint32_t bar) {
+__device__ __forceinline__ void commit_cg2_mc_elect(uint32_t bar, uint16_t mask = 3) {
   asm volatile(
       "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
       "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
-      ::"r"(bar), "h"((uint16_t)3)
+      ::"r"(bar), "h"(mask)
       : "memory");
 }
 
