@@ -247,11 +247,18 @@ def run_gpu(args, rank, world, local):
     if args.gemm_bn or args.gemm_stages:
         mm.mm_set_gemm_config(args.gemm_bn, args.gemm_stages, 0)
     pk = peaks()
-    nshard = args.config == "llama70b_down" and world > 1
-    comm = None
-    if nshard:
+    nshard = args.config == "llama70b_down" and (world > 1 or args.comm == "peer")
+    comm = win = y_peer = None
+    if nshard and args.comm == "nccl":
         from paper_2508_02343_b200.dist import exchange_unique_id
         comm = mm.mm_comm_init(rank, world, exchange_unique_id(mm.nccl_unique_id))
+    elif nshard:   # fused all-gather epilogue: tiles stored into every rank's Y over NVLink
+        if world > 1:
+            from paper_2508_02343_b200.dist import open_peer_window
+            win, y_peer = open_peer_window(M, N)
+        else:
+            buf = mm.peer_buffer(M, N, device=dev)
+            win, y_peer = mm.PeerWindow.from_ptrs(0, 1, [buf], M, N), mm.peer_y(buf, M, N)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     # bytes touched per step (for the L2 rotation count)
     per_set = 2 * M * K + M * K + (N // world if nshard else N) * K + 2 * M * N
@@ -265,6 +272,15 @@ def run_gpu(args, rank, world, local):
     stream = torch.cuda.Stream(dev)
     Ns = N // world if nshard else N
 
+    def gemm(st, y=None):
+        if nshard and win is not None:
+            mm.mm_mixed_gemm_bf16_nshard_peerstore(st["a"], st["wq"], plan, N, win, barrier=True, stream=stream)
+        elif nshard:
+            mm.mm_mixed_gemm_bf16_nshard_allgather(st["a"], st["wq"], plan, N, comm, out=st["y"] if y is None else y,
+                                                   stage=stage, stream=stream)
+        else:
+            mm.mm_mixed_gemm_bf16(st["a"], st["wq"], plan, out=st["y"] if y is None else y, stream=stream)
+
     def step(i, evs=None):
         s = sets[i % n_sets]
         if evs is not None:
@@ -272,11 +288,7 @@ def run_gpu(args, rank, world, local):
         mm.mm_reorder_quantize_act(s["x"], plan, out=s["a"], stream=stream)
         if evs is not None:
             evs[1].record(stream)
-        if nshard:
-            mm.mm_mixed_gemm_bf16_nshard_allgather(s["a"], s["wq"], plan, N, comm, out=s["y"], stage=stage,
-                                                   stream=stream)
-        else:
-            mm.mm_mixed_gemm_bf16(s["a"], s["wq"], plan, out=s["y"], stream=stream)
+        gemm(s)
         if evs is not None:
             evs[2].record(stream)
 
@@ -324,11 +336,7 @@ def run_gpu(args, rank, world, local):
             torch.cuda.synchronize()
             return k0.elapsed_time(k1) / args.steps
         rq_ms = kernel_pass(lambda st: mm.mm_reorder_quantize_act(st["x"], plan, out=st["a"], stream=stream))
-        if nshard:
-            gemm_ms = kernel_pass(lambda st: mm.mm_mixed_gemm_bf16_nshard_allgather(
-                st["a"], st["wq"], plan, N, comm, out=st["y"], stage=stage, stream=stream))
-        else:
-            gemm_ms = kernel_pass(lambda st: mm.mm_mixed_gemm_bf16(st["a"], st["wq"], plan, out=st["y"], stream=stream))
+        gemm_ms = kernel_pass(gemm)
         clocks = sampler.stop()
     total_ms = max_over_ranks(t0.elapsed_time(t1), world)
     ms = total_ms / args.steps
@@ -343,17 +351,13 @@ def run_gpu(args, rank, world, local):
     # ---- end to end through the public API with host buffers --------------------------
     x_host = sets[0]["x"].cpu().pin_memory()
     y_host = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
-    x_dev, y_dev = sets[0]["x"], sets[0]["y"]
+    x_dev, y_dev = sets[0]["x"], (y_peer if y_peer is not None else sets[0]["y"])
     with torch.cuda.stream(stream):
         def e2e_step():
             x_dev.copy_(x_host, non_blocking=True)
             mm.mm_reorder_quantize_act(x_dev, plan, out=sets[0]["a"], stream=stream)
-            if nshard:
-                mm.mm_mixed_gemm_bf16_nshard_allgather(sets[0]["a"], sets[0]["wq"], plan, N, comm, out=y_dev,
-                                                       stage=stage, stream=stream)
-            else:
-                mm.mm_mixed_gemm_bf16(sets[0]["a"], sets[0]["wq"], plan, out=y_dev, stream=stream)
-            y_host.copy_(y_dev, non_blocking=True)
+            gemm(sets[0], y_dev)
+            y_host.copy_(y_dev[:, :N] if y_dev.shape[1] != N else y_dev, non_blocking=True)
         for _ in range(max(3, args.warmup)):
             e2e_step()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -367,6 +371,11 @@ def run_gpu(args, rank, world, local):
         barrier(world)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
     e2e_val = units / (e2e_ms * 1e-3) / 1e12
+    if comm is not None:
+        mm.mm_comm_destroy(comm)
+    if win is not None:
+        barrier(world)   # no rank unmaps while a peer may still store into it
+        win.close()
 
     if rank != 0:
         return
@@ -382,7 +391,9 @@ def run_gpu(args, rank, world, local):
         "scaling": "strong" if nshard else "weak", "vs_baseline": None,
         "dtype": "mxfp4/mxfp6(e3m2)/mxfp8(e4m3) x e8m0, fp32 accum, bf16 out", "data": "synthetic",
         "config": {"workload": text, "M": M, "K": K, "N": N, "n4_n6_n8": list(n),
-                   "parallelism": (f"N-shard x{world} + NCCL all-gather" if nshard else
+                   "parallelism": ((f"N-shard x{world} + NCCL all-gather" if win is None else
+                                    f"N-shard x{world}, all-gather fused into the GEMM epilogue (peer stores)")
+                                   if nshard else
                                    ("replicas" if world > 1 else "1 GPU")),
                    "l2": f"{n_sets} rotating input/weight/output sets, {n_sets * per_set / 1e6:.0f} MB > L2 "
                          f"{l2 / 1e6:.0f} MB",
@@ -417,8 +428,7 @@ def run_gpu(args, rank, world, local):
         except Exception:
             pass
     print(json.dumps(out), flush=True)
-    if comm is not None:
-        mm.mm_comm_destroy(comm)
+
 
 
 def main():
@@ -428,6 +438,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="micromix", choices=["micromix", "reference"])
     ap.add_argument("--config", default="q_proj", choices=sorted(CONFIGS))
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
+                    help="N-shard output exchange: NCCL all-gather, or the fused peer-store epilogue")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gemm-bn", type=int, default=0, help="GEMM tile N override (tuning)")

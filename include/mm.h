@@ -230,6 +230,45 @@ mm_status mm_mixed_gemm_bf16_nshard_allgather(const mm_mx_tensor* a, const mm_mx
                                               void* d_y_full, int64_t ldy, void* d_stage,
                                               void* comm, mm_stream_t stream);
 
+/* ---- fused GEMM + all-gather epilogue over peer memory ----
+ * The N-shard of mm_mixed_gemm_bf16_nshard_allgather without a separate
+ * collective: every output tile of rank r is TMA-stored straight into EVERY
+ * rank's full Y (columns [r*Ns, (r+1)*Ns)) through peer-mapped memory over
+ * NVLink/NVSwitch, then a flag barrier tells each rank that all shards have
+ * landed.  Results equal the 1-GPU GEMM bit for bit (same tiles, same K order).
+ *
+ * Peer buffer (one per rank, caller-allocated, 256-B aligned, ZERO-FILLED before
+ * the handle exchange, e.g. torch.zeros): [Y: BF16 M x ldy, padded to 256 B]
+ * [flags: 64 x u32].  mm_peer_buffer_bytes gives its size.
+ *
+ * Window: this rank's table of all ranks' buffers.  mm_peer_window_open maps the
+ * peers' buffers from CUDA IPC handles (mm_ipc_get_handle on each rank, exchanged
+ * by the caller, e.g. through torch.distributed); mm_peer_window_from_ptrs takes
+ * device pointers valid in this process (already-mapped memory, or several
+ * "virtual ranks" on one GPU for testing).  world <= 8.  The window owns the IPC
+ * mappings it opened; mm_peer_window_close unmaps them (buffers stay the caller's).
+ *
+ * mm_mixed_gemm_bf16_nshard_peerstore: a = this rank's (replicated) activation,
+ * w_shard = its Ns = n_total / world weight rows, Ns % 16 == 0, ldy >= n_total,
+ * ldy % 8 == 0.  barrier = 1 appends the flag barrier on `stream` (the call then
+ * completes on every rank only when all ranks have called it: a collective);
+ * barrier = 0 leaves it to mm_peer_barrier (same-process virtual ranks, where the
+ * barriers of all ranks must run concurrently on different streams).  Errors as
+ * everywhere: validated before any launch, nothing enqueued on error. */
+size_t mm_peer_buffer_bytes(int64_t M, int64_t ldy);
+int32_t mm_ipc_handle_bytes(void);                                   /* 72 */
+mm_status mm_ipc_get_handle(const void* d_buf, void* h_handle_out);   /* 64 B CUDA IPC handle of the
+                                                                          allocation + u64 byte offset */
+mm_status mm_peer_window_open(int32_t rank, int32_t world, void* d_local_buf, const void* h_handles,
+                              int64_t M, int64_t ldy, void** win_out);
+mm_status mm_peer_window_from_ptrs(int32_t rank, int32_t world, void* const* h_dev_bufs, int64_t M,
+                                   int64_t ldy, void** win_out);
+mm_status mm_peer_window_close(void* win);
+mm_status mm_mixed_gemm_bf16_nshard_peerstore(const mm_mx_tensor* a, const mm_mx_tensor* w_shard,
+                                              const mm_plan* plan, int64_t n_total, void* win,
+                                              int32_t barrier, mm_stream_t stream);
+mm_status mm_peer_barrier(void* win, mm_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,7 +8,8 @@ is missing or the device is not sm_100, calls raise.
 Functions carry the C names:
     mm_plan_init, mm_calibrate_thresholds, mm_quantize_weight_offline,
     mm_reorder_quantize_act, mm_mixed_gemm_bf16, mm_reorder_act_bf16,
-    mm_comm_init, mm_mixed_gemm_bf16_nshard_allgather.
+    mm_comm_init, mm_mixed_gemm_bf16_nshard_allgather,
+    mm_mixed_gemm_bf16_nshard_peerstore (fused all-gather epilogue over peer memory).
 """
 from __future__ import annotations
 
@@ -37,6 +38,9 @@ EXPORTS = [
     "mm_comm_init", "mm_comm_destroy", "mm_mixed_gemm_bf16_nshard_allgather",
     "mm_calib_state_bytes", "mm_calib_accumulate", "mm_calib_finalize", "mm_plan_diagnostics",
     "mm_rmsnorm_reorder_quantize_act",
+    "mm_peer_buffer_bytes", "mm_ipc_handle_bytes", "mm_ipc_get_handle", "mm_peer_window_open",
+    "mm_peer_window_from_ptrs", "mm_peer_window_close", "mm_mixed_gemm_bf16_nshard_peerstore",
+    "mm_peer_barrier",
 ]
 
 
@@ -109,6 +113,14 @@ def lib(build_if_missing: bool = False):
             "mm_calib_finalize": (ctypes.c_int, [vp, i32, i32, i32, i32, vp, P, vp, vp, vp, vp]),
             "mm_plan_diagnostics": (ctypes.c_int, [P, vp, vp, ctypes.POINTER(CDiag)]),
             "mm_rmsnorm_reorder_quantize_act": (ctypes.c_int, [vp, i64, i64, vp, ctypes.c_double, P, X, vp]),
+            "mm_peer_buffer_bytes": (ctypes.c_size_t, [i64, i64]),
+            "mm_ipc_handle_bytes": (i32, []),
+            "mm_ipc_get_handle": (ctypes.c_int, [vp, vp]),
+            "mm_peer_window_open": (ctypes.c_int, [i32, i32, vp, vp, i64, i64, ctypes.POINTER(vp)]),
+            "mm_peer_window_from_ptrs": (ctypes.c_int, [i32, i32, ctypes.POINTER(vp), i64, i64, ctypes.POINTER(vp)]),
+            "mm_peer_window_close": (ctypes.c_int, [vp]),
+            "mm_mixed_gemm_bf16_nshard_peerstore": (ctypes.c_int, [X, X, P, i64, vp, i32, vp]),
+            "mm_peer_barrier": (ctypes.c_int, [vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -364,3 +376,66 @@ def shard_rows(N: int, world: int, rank: int):
     """Rows of W owned by `rank` under N-sharding (host logic, CPU-testable)."""
     from .dist import shard_rows as _sr
     return _sr(N, world, rank)
+
+
+# ---- fused GEMM + all-gather epilogue over peer memory (NEXT F1) ------------------
+def mm_peer_buffer_bytes(M: int, ldy: int) -> int:
+    return int(lib().mm_peer_buffer_bytes(M, ldy))
+
+
+def peer_buffer(M: int, ldy: int, device=None) -> torch.Tensor:
+    """A zero-filled peer buffer ([Y: BF16 M x ldy][flags]) as a uint8 tensor (256-B
+    aligned: the caching allocator aligns to 512 B)."""
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    return torch.zeros(mm_peer_buffer_bytes(M, ldy), dtype=torch.uint8, device=dev)
+
+
+def peer_y(buf: torch.Tensor, M: int, ldy: int) -> torch.Tensor:
+    """The BF16 [M, ldy] Y view of a peer buffer."""
+    return buf[: M * ldy * 2].view(torch.bfloat16).view(M, ldy)
+
+
+def ipc_handle(buf: torch.Tensor) -> bytes:
+    n = lib().mm_ipc_handle_bytes()
+    out = ctypes.create_string_buffer(n)
+    _check(lib().mm_ipc_get_handle(_ptr(buf), out))
+    return out.raw
+
+
+class PeerWindow:
+    """This rank's table of every rank's peer buffer (include/mm.h)."""
+
+    def __init__(self, handle, rank: int, world: int, M: int, ldy: int, keep=()):
+        self.h, self.rank, self.world, self.M, self.ldy = handle, rank, world, M, ldy
+        self._keep = keep   # buffers that must outlive the window
+
+    @classmethod
+    def open(cls, rank: int, world: int, local_buf: torch.Tensor, handles: list, M: int, ldy: int):
+        blob = b"".join(handles)
+        cbuf = ctypes.create_string_buffer(blob, len(blob))
+        h = ctypes.c_void_p()
+        _check(lib().mm_peer_window_open(rank, world, _ptr(local_buf), cbuf, M, ldy, ctypes.byref(h)))
+        return cls(h, rank, world, M, ldy, (local_buf,))
+
+    @classmethod
+    def from_ptrs(cls, rank: int, world: int, bufs: list, M: int, ldy: int):
+        arr = (ctypes.c_void_p * world)(*[b.data_ptr() for b in bufs])
+        h = ctypes.c_void_p()
+        _check(lib().mm_peer_window_from_ptrs(rank, world, arr, M, ldy, ctypes.byref(h)))
+        return cls(h, rank, world, M, ldy, tuple(bufs))
+
+    def close(self):
+        if self.h is not None:
+            _check(lib().mm_peer_window_close(self.h))
+            self.h = None
+
+
+def mm_mixed_gemm_bf16_nshard_peerstore(a: MXTensor, w_shard: MXTensor, plan: Plan, n_total: int,
+                                        win: PeerWindow, barrier: bool = True, stream=None):
+    _check(lib().mm_mixed_gemm_bf16_nshard_peerstore(ctypes.byref(a.c), ctypes.byref(w_shard.c),
+                                                     ctypes.byref(plan.c), n_total, win.h, int(barrier),
+                                                     _stream(stream)))
+
+
+def mm_peer_barrier(win: PeerWindow, stream=None):
+    _check(lib().mm_peer_barrier(win.h, _stream(stream)))

@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <mutex>
 
 #include "internal.h"
@@ -26,7 +27,43 @@ __global__ void gather_layout_kernel(const uint4* __restrict__ stage, int G, int
   }
 }
 
+// Flag barrier of a peer window (NEXT F1): thread j signals "rank `rank` is done" in
+// rank j's flag array (system-scope release, after a system fence so the preceding
+// GEMM's peer stores are performed first), then waits until rank j's flag in this
+// rank's array reaches `epoch` (system-scope acquire).  A peer that never arrives
+// traps after MM_PEER_TIMEOUT_NS instead of hanging the GPU.
+#ifndef MM_PEER_TIMEOUT_NS
+#define MM_PEER_TIMEOUT_NS 20000000000ull
+#endif
+__global__ void peer_barrier_kernel(PeerFlags fl, int rank, int world, uint32_t epoch) {
+  const int j = threadIdx.x;
+  if (j >= world) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(fl.f[j] + rank), "r"(epoch) : "memory");
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fl.f[rank] + j) : "memory");
+    if ((int32_t)(v - epoch) >= 0) break;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > MM_PEER_TIMEOUT_NS) {
+      printf("[mm peer barrier] rank %d: rank %d never arrived (epoch %u)\n", rank, j, epoch);
+      __trap();
+    }
+    __nanosleep(100);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_peer_barrier(const PeerFlags& fl, int rank, int world, uint32_t epoch, cudaStream_t s,
+                                int64_t* launches) {
+  peer_barrier_kernel<<<1, 32, 0, s>>>(fl, rank, world, epoch);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gather_layout(const uint16_t* stage, int G, int64_t M, int64_t Ns, uint16_t* y,
                                  int64_t ldy, cudaStream_t s, int64_t* launches) {

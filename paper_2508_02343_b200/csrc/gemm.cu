@@ -340,6 +340,13 @@ cudaError_t run(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_
 
 // 2-D K-major operand map: inner dim = K coordinate (bytes, or FP6 elements),
 // outer = rows; box = 128 x box_rows; 128-byte swizzle.
+static CUtensorMapL2promotion operand_l2_promotion() {
+  static const int v = [] { const char* e = getenv("MM_GEMM_L2PROMO"); return e ? atoi(e) : 3; }();
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                         : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 bool make_operand_map(CUtensorMap* m, const void* base, int g, int kp, int64_t rows, int64_t pitch,
                       int box_rows) {
   EncodeTiledFn enc = tensor_map_encoder();
@@ -354,7 +361,7 @@ bool make_operand_map(CUtensorMap* m, const void* base, int g, int kp, int64_t r
   cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_SWIZZLE_128B, operand_l2_promotion(),
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -393,6 +400,7 @@ cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStre
   int bn = cfg.block_n;
   // auto: CTA-pair 256 x 256 tiles once M fills a pair tile's rows, else single-CTA 128 x 256
   if (bn == 0) bn = a.M > 128 ? 512 : 256;
+  if (a.n_dst > 0) bn = 512;   // the fused all-gather epilogue lives in the CTA-pair kernel
   if (bn == 512) return launch_mixed_gemm_2cta(a, cfg, s, launches, err);
   if (bn == 128) {
     if (cfg.num_stages == 4) return run<128, 4>(a, cfg, s, launches, err);

@@ -63,10 +63,20 @@ constexpr int SF_COL = 464;
 template <int STAGES> __host__ __device__ constexpr int epi_nbuf() { return STAGES >= 6 ? 1 : 2; }
 template <int STAGES> __host__ __device__ constexpr int epi_bytes() { return 4 * epi_nbuf<STAGES>() * 32 * 64; }
 
+// Output tensor maps.  NP = 1: Y.  NP = kMaxPeers (NEXT F1, fused all-gather
+// epilogue): one map per rank of the peer window, each viewing THIS rank's column
+// slice [rank * Ns, (rank + 1) * Ns) of that rank's full Y, so every output tile is
+// stored straight into every rank's Y over NVLink and no separate all-gather runs.
+template <int NP>
+struct YMaps {
+  CUtensorMap m[NP];
+};
+
 struct Gemm2Dev {
   int64_t M, N;
   int num_m2, num_n, num_tiles;   // pair tiles of 256 x 256 (num_tiles counts cluster tiles)
   int num_nc;                     // cluster tile columns: ceil(num_n / CP)
+  int raster_g;                   // pair-row blocks per raster group (tile_coords)
   int nst0, nst1, nst2;           // stages per segment
   int n0, n1, n2;                 // real channels per segment
   int kp0, kp1, kp2;              // stored channels per segment
@@ -76,14 +86,15 @@ struct Gemm2Dev {
   int stream_k;                   // 1: stream-K split of the K loop over pairs (see work_item)
   float* ws;                      // stream-K partial tiles: [npairs][256 rows][256 cols] fp32
   int* ws_flag;                   // per pair: 8 epilogue warps arrive (+1), the finisher consumes (-1)
+  int ndst;  // output maps used (1, or the peer window's world size)
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
 };
 
 // Tile raster: groups of up to 8 pair-row blocks (2048 rows of A) sweep all of N
 // before moving on, so a wave of tiles reuses the same A rows from L2 (for large M
 // the whole A does not fit in L2, W of one layer does).
-__device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& mb2, int& nb) {
-  const int G = num_m2 < 8 ? num_m2 : 8;
+__device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& mb2, int& nb, int rg) {
+  const int G = num_m2 < rg ? num_m2 : rg;
   const int per_group = G * num_n;
   const int grp = t / per_group, r = t - grp * per_group;
   const int rows = min(G, num_m2 - grp * G);
@@ -140,7 +151,7 @@ __device__ __forceinline__ void seg_stage(const Gemm2Dev& p, int j, int& kcoord,
 // CTA.  Every CTA's smem stage is then written by two producers, so a stage is free
 // only when BOTH pairs' MMAs have consumed it: the empty barriers count CP commits,
 // and each leader's per-stage commit is multicast to all 2 * CP CTAs.
-template <int STAGES, int CP>
+template <int STAGES, int CP, int NP>
 __global__ void __launch_bounds__(kThreads2, 1)
 mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                 const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb0,
@@ -148,7 +159,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
                 const __grid_constant__ CUtensorMap tsa0, const __grid_constant__ CUtensorMap tsa1,
                 const __grid_constant__ CUtensorMap tsa2, const __grid_constant__ CUtensorMap tsb0,
                 const __grid_constant__ CUtensorMap tsb1, const __grid_constant__ CUtensorMap tsb2,
-                const __grid_constant__ CUtensorMap ty, const __grid_constant__ Gemm2Dev p) {
+                const __grid_constant__ YMaps<NP> tys, const __grid_constant__ Gemm2Dev p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -219,7 +230,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         int t, s0, s1;
         work_item(p, pair, npairs, S, it, t, s0, s1);
         int mb2, nb;
-        tile_coords(t, num_m2, p.num_nc, mb2, nb);
+        tile_coords(t, num_m2, p.num_nc, mb2, nb, p.raster_g);
         nb = nb * CP + pp;
         const int m0 = mb2 * 256 + 128 * (int)rank;      // this CTA's A rows
         const int n0 = nb * 256 + 128 * (int)rank;       // this CTA's W rows (its half of N)
@@ -391,7 +402,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       int t, s0, s1;
       work_item(p, pair, npairs, S, it, t, s0, s1);
       int mb2, nb;
-      tile_coords(t, num_m2, p.num_nc, mb2, nb);
+      tile_coords(t, num_m2, p.num_nc, mb2, nb, p.raster_g);
       nb = nb * CP + pp;
       const bool dead = nb >= p.num_n;   // CP = 2 with odd num_n: the second pair's tile is past N
       // stream-K roles of this item: leave a partial (head of a tile) / add one (tail)
@@ -412,9 +423,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       const int row0 = mb2 * 256 + 128 * (int)rank + q * 32;
       const int n0 = nb * 256;
       const uint32_t acc_col = acc ? ACC1_COL : 0;
-#pragma unroll 1
       uint32_t rn[32];   // chunk 1 of the drain order, loaded together with chunk 0
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc_col;
+#pragma unroll 1
       for (int i = 0; i < 8; ++i) {
         // acc0: its overlap (columns 208..255) lives in chunks 6, 7 -> drain those first;
         // acc1: its overlap is its own columns 0..47 -> chunks 0, 1 come first anyway.
@@ -476,7 +487,11 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          ptx::tma_store_2d(&ty, ptx::smem_u32(buf), n0 + 32 * c, row0);
+          if constexpr (NP == 1) {
+            ptx::tma_store_2d(&tys.m[0], ptx::smem_u32(buf), n0 + 32 * c, row0);
+          } else {
+            for (int dst = 0; dst < p.ndst; ++dst) ptx::tma_store_2d(&tys.m[dst], ptx::smem_u32(buf), n0 + 32 * c, row0);
+          }
           ptx::bulk_commit_group();
         }
         ++nstore;
@@ -491,7 +506,10 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         if (lane == 0) atomicSub(p.ws_flag + (pair - 1), 1);
       }
     }
-    if (lane == 0) ptx::bulk_wait_group_read<0>();
+    if (lane == 0) {
+      if constexpr (NP == 1) ptx::bulk_wait_group_read<0>();
+      else ptx::bulk_wait_group<0>();   // peer stores fully performed before the CTA retires
+    }
     if (trace && q == 0) g_trace[blockIdx.x][12] = ptx::globaltimer_ns();
   }
 
@@ -544,9 +562,10 @@ bool stream_k_workspace(cudaStream_t s, int npairs, float** ws, int** flags) {
   return true;
 }
 
-template <int STAGES, int CP>
+template <int STAGES, int CP, int NP>
 cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches, const char** err) {
-  CUtensorMap maps[13];
+  CUtensorMap maps[12];
+  YMaps<NP> ym;
   int first = -1;
   for (int g = 0; g < 3; ++g) {
     if (a.geom.n[g] == 0) continue;
@@ -564,19 +583,24 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   for (int g = 0; g < 3; ++g)
     if (a.geom.n[g] == 0)
       for (int k = 0; k < 4; ++k) maps[3 * k + g] = maps[3 * k + first];   // valid, never used
-  {  // Y [M, N] BF16 row-major (ld = ldy): TMA store boxes of 32 rows x 32 columns
+  // Y [M, N] BF16 row-major (ld = ldy): TMA store boxes of 32 rows x 32 columns; in
+  // peer mode one map per destination rank (its Y + this rank's column offset).
+  const int ndst = NP == 1 ? 1 : a.n_dst;
+  for (int dst = 0; dst < ndst; ++dst) {
     EncodeTiledFn enc = tensor_map_encoder();
     cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
     cuuint64_t strides[1] = {(cuuint64_t)a.ldy * 2};
     cuuint32_t box[2] = {32, 32};
     cuuint32_t estr[2] = {1, 1};
-    if (!enc || enc(&maps[12], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, a.y, dims, strides, box, estr,
+    uint16_t* base = NP == 1 ? a.y : a.y_dst[dst] + a.y_col_off;
+    if (!enc || enc(&ym.m[dst], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
       *err = "cuTensorMapEncodeTiled(Y) failed";
       return cudaErrorInvalidValue;
     }
   }
+  for (int dst = ndst; dst < NP; ++dst) ym.m[dst] = ym.m[0];   // valid, never used
   Gemm2Dev p{};
   p.M = a.M;
   p.N = a.N;
@@ -584,6 +608,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.num_n = (int)((a.N + 255) / 256);
   p.num_nc = (p.num_n + CP - 1) / CP;
   p.num_tiles = p.num_m2 * p.num_nc;
+  { const char* e = getenv("MM_GEMM_RASTER_G"); p.raster_g = e ? atoi(e) : 8; if (p.raster_g < 1) p.raster_g = 1; }
   p.nst0 = (a.geom.kp[0] + 255) / 256;
   p.nst1 = a.geom.kp[1] / 128;
   p.nst2 = a.geom.kp[2] / 128;
@@ -594,12 +619,15 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.idesc2 = make_idesc_mn(a.geom.fmt[2], 2, 256, 256);
   p.y = a.y;
   p.ldy = a.ldy;
+  p.ndst = ndst;
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   if (p.num_tiles == 0) return cudaSuccess;
   int grid = sm_count() / (2 * CP) * (2 * CP);
   if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas / (2 * CP) * (2 * CP);
   if (grid < 2 * CP) grid = 2 * CP;
   if (grid > 2 * CP * p.num_tiles) grid = 2 * CP * p.num_tiles;
+  static const bool nonpersist = [] { const char* e = getenv("MM_GEMM_NONPERSIST"); return e && atoi(e); }();
+  if (nonpersist) grid = 2 * CP * p.num_tiles;   // experiment: one tile per pair, hardware scheduling
   // Stream-K when the last wave of tiles would be ragged and there are only a few
   // waves (each pair then finishes at most one tile left by its neighbour).
   const int npairs = grid / 2;   // (stream-K: CP = 1 only)
@@ -617,7 +645,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   }
   const size_t smem =
       1024 + (size_t)STAGES * STAGE_BYTES + NSF * SFG_BYTES + epi_bytes<STAGES>() + (2 * STAGES + 6 + NSF) * 8 + 16;
-  auto kern = mixgemm2_kernel<STAGES, CP>;
+  auto kern = mixgemm2_kernel<STAGES, CP, NP>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
   if (p.dbg & 128) {   // diagnostics: co-resident clusters of this configuration
@@ -638,7 +666,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
             cudaGetErrorString(oe));
   }
   e = launch_pdl_cluster(kern, dim3(grid), dim3(kThreads2), smem, s, 2 * CP, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
-                 maps[6], maps[7], maps[8], maps[9], maps[10], maps[11], maps[12], p);
+                 maps[6], maps[7], maps[8], maps[9], maps[10], maps[11], ym, p);
   if (launches) ++*launches;
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -667,13 +695,14 @@ cudaError_t launch_mixed_gemm_2cta(const GemmArgs& a, const GemmConfig& cfg, cud
   if (c == 2 && num_n % 2 && cp_env != 2) c = 1;
   static const int st_env = [] { const char* e = getenv("MM_GEMM_STAGES"); return e ? atoi(e) : 0; }();
   const int st = cfg.num_stages ? cfg.num_stages : (st_env ? st_env : 5);
+  if (a.n_dst > 0) return run2<5, 1, kMaxPeers>(a, cfg, s, launches, err);   // fused all-gather epilogue
   if (c == 1) {
-    if (st == 4) return run2<4, 1>(a, cfg, s, launches, err);
-    if (st == 6) return run2<6, 1>(a, cfg, s, launches, err);
-    return run2<5, 1>(a, cfg, s, launches, err);
+    if (st == 4) return run2<4, 1, 1>(a, cfg, s, launches, err);
+    if (st == 6) return run2<6, 1, 1>(a, cfg, s, launches, err);
+    return run2<5, 1, 1>(a, cfg, s, launches, err);
   }
-  if (cfg.num_stages == 4) return run2<4, 2>(a, cfg, s, launches, err);
-  return run2<5, 2>(a, cfg, s, launches, err);
+  if (cfg.num_stages == 4) return run2<4, 2, 1>(a, cfg, s, launches, err);
+  return run2<5, 2, 1>(a, cfg, s, launches, err);
 }
 
 }  // namespace mmx

@@ -68,7 +68,13 @@ struct GemmArgs {
   const uint8_t* w_sf[3];
   uint16_t* y;   // BF16 [M, ldy]
   int64_t ldy;
+  // Fused all-gather epilogue (NEXT F1): n_dst > 0 stores every tile into each
+  // y_dst[d] + y_col_off (the ranks' full Y buffers, this rank's column slice).
+  int n_dst = 0;
+  uint16_t* y_dst[8] = {};
+  int64_t y_col_off = 0;
 };
+constexpr int kMaxPeers = 8;
 
 struct GemmConfig {
   int block_n = 0;      // 0 = auto
@@ -85,6 +91,14 @@ cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStre
 // [G][M][Ns] -> [M][G*Ns] layout fix after the all-gather (comm.cu).
 cudaError_t launch_gather_layout(const uint16_t* stage, int G, int64_t M, int64_t Ns,
                                  uint16_t* y, int64_t ldy, cudaStream_t s, int64_t* launches);
+
+// Peer-window flag arrays (one per rank, mapped into this process) and the barrier
+// that follows a fused all-gather GEMM (comm.cu).
+struct PeerFlags {
+  uint32_t* f[kMaxPeers];
+};
+cudaError_t launch_peer_barrier(const PeerFlags& fl, int rank, int world, uint32_t epoch, cudaStream_t s,
+                                int64_t* launches);
 
 int sm_count();
 

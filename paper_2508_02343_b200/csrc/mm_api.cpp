@@ -474,8 +474,21 @@ mm_status mm_reorder_act_bf16(const void* d_x, int64_t M, int64_t ldx, const mm_
   return MM_OK;
 }
 
+// Peer window of the fused all-gather epilogue (NEXT F1).
+struct MmPeerWin {
+  int rank = 0, world = 0;
+  int64_t M = 0, ldy = 0;
+  uint16_t* y[kMaxPeers] = {};
+  uint32_t* flags[kMaxPeers] = {};
+  void* ipc_base[kMaxPeers] = {};   // mappings opened by mm_peer_window_open (unmapped on close)
+  uint32_t epoch = 0;
+};
+
+static size_t peer_y_bytes(int64_t M, int64_t ldy) { return ((size_t)M * (size_t)ldy * 2 + 255) / 256 * 256; }
+
 static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const mm_plan* plan, void* d_y,
-                             int64_t ldy, int64_t n_cols, mm_stream_t stream, bool no_stream_k = false) {
+                             int64_t ldy, int64_t n_cols, mm_stream_t stream, bool no_stream_k = false,
+                             const MmPeerWin* win = nullptr) {
   mm_status st = check_device();
   if (st != MM_OK) return st;
   if ((st = validate_plan(plan)) != MM_OK) return st;
@@ -502,6 +515,11 @@ static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const
   }
   ga.y = static_cast<uint16_t*>(d_y);
   ga.ldy = ldy;
+  if (win) {
+    ga.n_dst = win->world;
+    for (int r = 0; r < win->world; ++r) ga.y_dst[r] = win->y[r];
+    ga.y_col_off = (int64_t)win->rank * N;
+  }
   GemmConfig cfg;
   {
     std::lock_guard<std::mutex> lk(g_cfg_mu);
@@ -587,6 +605,141 @@ mm_status mm_mixed_gemm_bf16_nshard_allgather(const mm_mx_tensor* a, const mm_mx
   if (r != ncclSuccess) return fail(MM_ERR_NCCL, "ncclAllGather: %s", api.errStr(r));
   cudaError_t e = launch_gather_layout(stage, c->world, M, Ns, static_cast<uint16_t*>(d_y_full), ldy, s, &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "layout launch");
+  return MM_OK;
+}
+
+size_t mm_peer_buffer_bytes(int64_t M, int64_t ldy) {
+  if (M < 0 || ldy < 0) return 0;
+  return peer_y_bytes(M, ldy) + 64 * sizeof(uint32_t);
+}
+
+// IPC handle of the allocation containing d_buf + the byte offset of d_buf inside it
+// (caching allocators such as PyTorch's sub-allocate cudaMalloc blocks).
+int32_t mm_ipc_handle_bytes(void) { return (int32_t)(sizeof(cudaIpcMemHandle_t) + sizeof(uint64_t)); }
+
+mm_status mm_ipc_get_handle(const void* d_buf, void* h_handle_out) {
+  if (!d_buf || !h_handle_out) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) ? reinterpret_cast<RangeFn>(p) : nullptr;
+  }();
+  if (!range) return fail(MM_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(d_buf)) != CUDA_SUCCESS)
+    return fail(MM_ERR_INVALID_ARGUMENT, "d_buf is not device memory");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  const uint64_t off = (uint64_t)(reinterpret_cast<CUdeviceptr>(d_buf) - base);
+  std::memcpy(h_handle_out, &h, sizeof(h));
+  std::memcpy(static_cast<uint8_t*>(h_handle_out) + sizeof(h), &off, sizeof(off));
+  return MM_OK;
+}
+
+static mm_status peer_window_check(int32_t rank, int32_t world, int64_t M, int64_t ldy) {
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+    return fail(MM_ERR_INVALID_ARGUMENT, "rank %d / world %d (world must be 1..%d)", rank, world, kMaxPeers);
+  if (M < 0 || ldy < 0 || ldy % 8 != 0) return fail(MM_ERR_SHAPE, "bad M / ldy (ldy %% 8 == 0)");
+  return MM_OK;
+}
+
+mm_status mm_peer_window_from_ptrs(int32_t rank, int32_t world, void* const* h_dev_bufs, int64_t M, int64_t ldy,
+                                   void** win_out) {
+  mm_status st = peer_window_check(rank, world, M, ldy);
+  if (st != MM_OK) return st;
+  if (!h_dev_bufs || !win_out) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  for (int r = 0; r < world; ++r)
+    if (!h_dev_bufs[r] || !aligned(h_dev_bufs[r], 256)) return fail(MM_ERR_ALIGNMENT, "buffer %d: NULL or not 256-B aligned", r);
+  MmPeerWin* w = new MmPeerWin;
+  w->rank = rank;
+  w->world = world;
+  w->M = M;
+  w->ldy = ldy;
+  for (int r = 0; r < world; ++r) {
+    w->y[r] = static_cast<uint16_t*>(h_dev_bufs[r]);
+    w->flags[r] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(h_dev_bufs[r]) + peer_y_bytes(M, ldy));
+  }
+  *win_out = w;
+  return MM_OK;
+}
+
+mm_status mm_peer_window_open(int32_t rank, int32_t world, void* d_local_buf, const void* h_handles, int64_t M,
+                              int64_t ldy, void** win_out) {
+  mm_status st = peer_window_check(rank, world, M, ldy);
+  if (st != MM_OK) return st;
+  if (!d_local_buf || !h_handles || !win_out) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!aligned(d_local_buf, 256)) return fail(MM_ERR_ALIGNMENT, "local buffer must be 256-B aligned");
+  void* bufs[kMaxPeers] = {};
+  void* bases[kMaxPeers] = {};   // opened IPC mappings (allocation bases)
+  bool opened[kMaxPeers] = {};
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) { bufs[r] = d_local_buf; continue; }
+    cudaIpcMemHandle_t h;
+    uint64_t off = 0;
+    const uint8_t* rec = static_cast<const uint8_t*>(h_handles) + (size_t)r * (sizeof(h) + sizeof(off));
+    std::memcpy(&h, rec, sizeof(h));
+    std::memcpy(&off, rec + sizeof(h), sizeof(off));
+    cudaError_t e = cudaIpcOpenMemHandle(&bases[r], h, cudaIpcMemLazyEnablePeerAccess);
+    if (e == cudaSuccess) bufs[r] = static_cast<uint8_t*>(bases[r]) + off;
+    if (e != cudaSuccess) {
+      for (int q = 0; q < r; ++q)
+        if (opened[q]) cudaIpcCloseMemHandle(bases[q]);
+      return cuda_fail(e, "cudaIpcOpenMemHandle");
+    }
+    opened[r] = true;
+  }
+  void* win = nullptr;
+  st = mm_peer_window_from_ptrs(rank, world, bufs, M, ldy, &win);
+  if (st != MM_OK) {
+    for (int q = 0; q < world; ++q)
+      if (opened[q]) cudaIpcCloseMemHandle(bases[q]);
+    return st;
+  }
+  for (int q = 0; q < world; ++q) static_cast<MmPeerWin*>(win)->ipc_base[q] = opened[q] ? bases[q] : nullptr;
+  *win_out = win;
+  return MM_OK;
+}
+
+mm_status mm_peer_window_close(void* win) {
+  if (!win) return MM_OK;
+  MmPeerWin* w = static_cast<MmPeerWin*>(win);
+  for (int r = 0; r < w->world; ++r)
+    if (w->ipc_base[r]) cudaIpcCloseMemHandle(w->ipc_base[r]);
+  delete w;
+  return MM_OK;
+}
+
+mm_status mm_peer_barrier(void* win, mm_stream_t stream) {
+  if (!win) return fail(MM_ERR_INVALID_ARGUMENT, "NULL window");
+  mm_status st = check_device();
+  if (st != MM_OK) return st;
+  MmPeerWin* w = static_cast<MmPeerWin*>(win);
+  PeerFlags fl{};
+  for (int r = 0; r < w->world; ++r) fl.f[r] = w->flags[r];
+  const uint32_t epoch = ++w->epoch;
+  cudaError_t e = launch_peer_barrier(fl, w->rank, w->world, epoch, reinterpret_cast<cudaStream_t>(stream), &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "peer barrier launch");
+  return MM_OK;
+}
+
+mm_status mm_mixed_gemm_bf16_nshard_peerstore(const mm_mx_tensor* a, const mm_mx_tensor* w_shard,
+                                              const mm_plan* plan, int64_t n_total, void* win, int32_t barrier,
+                                              mm_stream_t stream) {
+  if (!win || !a || !w_shard) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  MmPeerWin* w = static_cast<MmPeerWin*>(win);
+  const int64_t Ns = w_shard->rows;
+  if (Ns * w->world != n_total) return fail(MM_ERR_SHAPE, "shard rows * world != n_total");
+  if (Ns % 16 != 0) return fail(MM_ERR_SHAPE, "shard rows must be a multiple of 16");
+  if (a->rows != w->M) return fail(MM_ERR_SHAPE, "activation rows %lld != window M %lld", (long long)a->rows, (long long)w->M);
+  if (w->ldy < n_total) return fail(MM_ERR_SHAPE, "window ldy < n_total");
+  mm_status st = gemm_common(a, w_shard, plan, w->y[w->rank] + (int64_t)w->rank * Ns, w->ldy, Ns, stream,
+                             /*no_stream_k=*/true, w);
+  if (st != MM_OK) return st;
+  if (barrier) return mm_peer_barrier(win, stream);
   return MM_OK;
 }
 

@@ -50,3 +50,26 @@ def gathered_to_row_major(stage: torch.Tensor, world: int, M: int, Ns: int) -> t
     """Reference statement of the layout the library's gather_layout kernel
     produces: stage [G][M][Ns] -> Y [M][G*Ns] (used by the CPU tests)."""
     return stage.view(world, M, Ns).permute(1, 0, 2).reshape(M, world * Ns)
+
+
+def exchange_handles(handle: bytes, group=None) -> list:
+    """All ranks' IPC handles in rank order (NEXT F1 peer window; any backend)."""
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, handle, group=group)
+    if any(not isinstance(h, (bytes, bytearray)) or len(h) != len(handle) for h in out):
+        raise RuntimeError("peer handle exchange: malformed handle")
+    return [bytes(h) for h in out]
+
+
+def open_peer_window(M: int, ldy: int, group=None):
+    """Collective: allocate this rank's zero-filled peer buffer, exchange IPC handles
+    through the process group and map every peer's buffer.  Returns (window, Y view
+    of the local buffer).  The zero fill is complete before the handles leave this
+    rank, so no peer can signal into a flag array that is cleared later."""
+    import paper_2508_02343_b200 as mm
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    buf = mm.peer_buffer(M, ldy)
+    torch.cuda.synchronize()
+    handles = exchange_handles(mm.ipc_handle(buf), group)
+    win = mm.PeerWindow.open(rank, world, buf, handles, M, ldy)
+    return win, mm.peer_y(buf, M, ldy)

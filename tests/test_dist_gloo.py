@@ -48,11 +48,19 @@ def _worker(rank, world, port, q):
         y = mmdist.gathered_to_row_major(stage, world, M, N // world)
         uid = mmdist.exchange_unique_id(lambda: bytes(range(128)))
         t = mmdist.max_over_ranks(1.0 + rank)
+        # peer-window handle exchange (fused all-gather epilogue): rank order kept
+        hs = mmdist.exchange_handles(bytes([rank + 1]) * 72)
+        hs_ok = hs == [bytes([r + 1]) * 72 for r in range(world)]
+        try:   # a rank with a malformed handle makes every rank fail loudly
+            mmdist.exchange_handles(bytes([rank + 1]) * (72 if rank == 0 else 8))
+            bad_ok = False
+        except RuntimeError:
+            bad_ok = True
         if rank == 0:
             _, full = ogemm.mixed_linear_ref(x, bf16_bits(w), cal["perm"], cal["n"])
-            q.put(("ok", bool(np.array_equal(y.numpy(), full)), uid == bytes(range(128)), t))
+            q.put(("ok", bool(np.array_equal(y.numpy(), full)), uid == bytes(range(128)), t, hs_ok and bad_ok))
         else:
-            q.put(("rank1", uid == bytes(range(128)), t))
+            q.put(("rank1", uid == bytes(range(128)), t, hs_ok and bad_ok))
     except Exception as e:  # pragma: no cover - reported through the queue
         q.put(("err", repr(e)))
     finally:
@@ -77,6 +85,7 @@ def test_nshard_allgather_equals_unsharded_gloo():
     assert r0[1], "sharded + gathered Y differs from the unsharded oracle"
     assert r0[2] and r1[1], "unique id not exchanged"
     assert r0[3] == 2.0 and r1[2] == 2.0
+    assert r0[4] and r1[3], "peer handle exchange lost rank order or accepted a malformed handle"
 
 
 def test_shard_rows():
