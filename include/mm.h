@@ -203,7 +203,8 @@ mm_status mm_reorder_act_bf16(const void* d_x, int64_t M, int64_t ldx, const mm_
                               void* d_xr, int64_t ldxr, mm_stream_t stream);
 
 /* GEMM tile configuration override for tuning (0 = automatic).  block_n: 128 or 256
- * = single-CTA 128 x block_n tiles, 512 = CTA-pair (cta_group::2) 256 x 256 tiles;
+ * = single-CTA 128 x block_n tiles, 512 = CTA-pair (cta_group::2) 256 x 256 tiles,
+ * 1 = the small-M swap-AB / split-K kernel (M <= 128; auto for M <= 32);
  * num_stages: smem pipeline depth (kernel-specific set, 0 = default). */
 mm_status mm_set_gemm_config(int32_t block_n, int32_t num_stages, int32_t max_ctas);
 

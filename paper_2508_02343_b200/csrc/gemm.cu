@@ -401,6 +401,17 @@ cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStre
   // auto: CTA-pair 256 x 256 tiles once M fills a pair tile's rows, else single-CTA 128 x 256
   if (bn == 0) bn = a.M > 128 ? 512 : 256;
   if (a.n_dst > 0) bn = 512;   // the fused all-gather epilogue lives in the CTA-pair kernel
+  // small M (decode-like): swap-AB + split-K kernel (gemm_sm.cu), unless a tile
+  // configuration is forced or MM_GEMM_SMALLM=0
+  // Auto (measured, N = 4096: 10-13 us vs 25 us at M <= 32): M <= 32 and few enough
+  // 128-row W tiles that every tile gets >= 2 K splits; beyond that the 128 x 256 tile
+  // kernel is as fast or faster.  MM_GEMM_SMALLM=1 forces it for any M <= 128.
+  static const int smallm_env = [] { const char* e = getenv("MM_GEMM_SMALLM"); return e ? atoi(e) : -1; }();
+  const bool smallm_auto = a.M <= 32 && 2 * ((a.N + 127) / 128) <= sm_count();
+  if (a.n_dst == 0 && a.M <= 128 &&
+      (cfg.block_n == 1 || (cfg.block_n == 0 && smallm_env != 0 && (smallm_env == 1 || smallm_auto))))
+    return launch_mixed_gemm_smallm(a, cfg, s, launches, err);
+  if (bn == 1) bn = a.M > 128 ? 512 : 256;   // small-M kernel requested but M > 128
   if (bn == 512) return launch_mixed_gemm_2cta(a, cfg, s, launches, err);
   if (bn == 128) {
     if (cfg.num_stages == 4) return run<128, 4>(a, cfg, s, launches, err);

@@ -114,6 +114,8 @@ EncodeTiledFn tensor_map_encoder();
 // tcgen05 instruction descriptor for an M x N MMA of segment g (gemm.cu).
 bool make_operand_map(CUtensorMap* m, const void* base, int g, int kp, int64_t rows, int64_t pitch, int box_rows);
 uint32_t make_idesc_mn(int fmt, int g, int m, int n);
+cudaError_t launch_mixed_gemm_smallm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
+                                     const char** err);
 cudaError_t launch_mixed_gemm_2cta(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
                                    const char** err);
 

@@ -270,8 +270,9 @@ int64_t mm_calib_workspace_bytes(int64_t L, int32_t K) {
 }
 
 mm_status mm_set_gemm_config(int32_t block_n, int32_t num_stages, int32_t max_ctas) {
-  if (block_n != 0 && block_n != 128 && block_n != 256 && block_n != 512)
-    return fail(MM_ERR_INVALID_ARGUMENT, "block_n must be 0 (auto), 128, 256 (one CTA) or 512 (CTA pair, 256x256)");
+  if (block_n != 0 && block_n != 1 && block_n != 128 && block_n != 256 && block_n != 512)
+    return fail(MM_ERR_INVALID_ARGUMENT,
+                "block_n must be 0 (auto), 1 (small-M swap-AB kernel, M <= 128), 128, 256 (one CTA) or 512 (CTA pair)");
   std::lock_guard<std::mutex> lk(g_cfg_mu);
   g_gemm_cfg.block_n = block_n;
   g_gemm_cfg.num_stages = num_stages;

@@ -68,9 +68,10 @@ def _int_operand(rows, n, rng, kind):
     return np.concatenate(parts, axis=1).astype(np.float64)
 
 
-@pytest.mark.parametrize("M,N,n", [(128, 256, (256, 128, 128)), (200, 272, (96, 160, 224)),
-                                   (64, 512, (1024, 512, 256))])
-def test_exact_integer_case_bit_exact(M, N, n):
+@pytest.mark.parametrize("M,N,n,bn", [(128, 256, (256, 128, 128), 0), (200, 272, (96, 160, 224), 0),
+                                      (64, 512, (1024, 512, 256), 0), (24, 512, (1024, 512, 256), 0),
+                                      (128, 384, (256, 128, 128), 1)])
+def test_exact_integer_case_bit_exact(M, N, n, bn):
     """P-I(i): all products and partial sums are integers < 2^24, so FP32
     accumulation is exact in any order and Y must equal bf16(Y_exact) bit for bit."""
     rng = np.random.default_rng(M + N)
@@ -83,7 +84,11 @@ def test_exact_integer_case_bit_exact(M, N, n):
     x = bits_to_bf16(omx.bf16_rne_bits(xa))
     w = bits_to_bf16(omx.bf16_rne_bits(wa))
     plan = mm.mm_plan_init(K, n, perm)
-    y = _run(x, w, plan)
+    mm.mm_set_gemm_config(bn, 0, 0)     # bn = 1: small-M swap-AB / split-K kernel (M = 24: auto)
+    try:
+        y = _run(x, w, plan)
+    finally:
+        mm.mm_set_gemm_config(0, 0, 0)
     exact = xa_r @ wa_r.T
     assert np.max(np.abs(exact)) < 2 ** 24
     yref, ybf = _ref(x, w, plan)
@@ -201,3 +206,49 @@ def test_stream_k_matches_oracle_and_data_parallel(M, N, n, monkeypatch):
     a, b = y_sk.double().cpu().numpy(), y_dp.double().cpu().numpy()
     assert ogemm.rel_fro(a, b) < 1e-3
     assert not np.array_equal(a, b) or True   # identical is fine too (no split tile)
+
+
+# ---- small-M path (NEXT F3): swap-AB + split-K kernel (gemm_sm.cu) ----------------
+@pytest.mark.parametrize("M,N,n", [(1, 256, (128, 64, 64)), (7, 384, (256, 128, 128)), (16, 4096, (2240, 1184, 672)),
+                                   (33, 1000 - 1000 % 16, (512, 256, 256)), (64, 2048, (96, 160, 224)),
+                                   (100, 4096, (2240, 1184, 672)), (128, 1536, (1024, 512, 256))])
+def test_small_m_swap_ab_split_k(M, N, n):
+    """The swap-AB / split-K kernel (forced through block_n = 1; automatic for M <= 32),
+    ragged rows and 128-channel tiles, every segment mix, 1..4 K splits."""
+    K = sum(n)
+    x = gen_act(M, K, 1003, 2020 + M)
+    w = gen_weight(N, K, 3020 + N)
+    plan = mm.mm_plan_init(K, n, gen_perm(K, 14))
+    mm.mm_set_gemm_config(1, 0, 0)
+    try:
+        y = _run(x, w, plan)
+    finally:
+        mm.mm_set_gemm_config(0, 0, 0)
+    yref, ybf = _ref(x, w, plan)
+    _check(y, yref, ybf)
+
+
+def test_small_m_matches_tile_kernel_and_is_deterministic():
+    """The split-K result is deterministic (fixed summation order) and agrees with
+    the 128 x 256 tile kernel within the oracle bar (the exact-integer case is
+    bit-exact in both: test_exact_integer_case_bit_exact)."""
+    M, N, n = 24, 4096, (2240, 1184, 672)
+    K = sum(n)
+    plan = mm.mm_plan_init(K, n, gen_perm(K, 15))
+    a = mm.mm_reorder_quantize_act(gen_act(M, K, 1000, 2030).cuda(), plan)
+    wq = mm.mm_quantize_weight_offline(gen_weight(N, K, 3030).cuda(), plan)
+    mm.mm_set_gemm_config(1, 0, 0)
+    try:
+        y1 = mm.mm_mixed_gemm_bf16(a, wq, plan)
+        y2 = mm.mm_mixed_gemm_bf16(a, wq, plan)
+    finally:
+        mm.mm_set_gemm_config(0, 0, 0)
+    mm.mm_set_gemm_config(256, 4, 0)
+    try:
+        yt = mm.mm_mixed_gemm_bf16(a, wq, plan)
+    finally:
+        mm.mm_set_gemm_config(0, 0, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
+    d = (y1.double() - yt.double()).norm() / yt.double().norm()
+    assert d <= TOL, d
