@@ -125,6 +125,18 @@ def c2():
     return [measure_layer("C2 Llama-3.1-8B q_proj", 2048, 4096, 4096, plan)]
 
 
+def c6():
+    """Decode-like small M (NEXT F3 small-M path): Llama-3.1-8B q_proj and down_proj
+    at M = 1 / 16 / 32 / 128 (W read once from HBM is the bound)."""
+    out = []
+    plan_h = calibrated_plan(4096, layer=0)
+    plan_d = calibrated_plan(14336, layer=2)
+    for M in (1, 16, 32, 128):
+        out.append(measure_layer(f"C6 decode q_proj M={M}", M, 4096, 4096, plan_h, sets=8))
+        out.append(measure_layer(f"C6 decode down M={M}", M, 14336, 4096, plan_d, sets=8))
+    return out
+
+
 def c3(batches=(1, 8, 32)):
     out = []
     plan_h = calibrated_plan(4096, layer=0)      # input of qkv and gate_up (post-norm hidden)
@@ -160,7 +172,7 @@ def c5():
 def main():
     global L2
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-    which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["c1", "c2", "c3", "c4", "c5"]
+    which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["c1", "c2", "c3", "c4", "c5", "c6"]
     torch.cuda.set_device(0)
     L2 = torch.cuda.get_device_properties(0).L2_cache_size
     res = []
