@@ -324,10 +324,10 @@ cudaError_t run_sm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int
   p.ldy = a.ldy;
   if (p.num_nt == 0 || a.M == 0) return cudaSuccess;
   // splits: fill the SMs once (one CTA per SM), at least 2 stages per unit; only
-  // for M <= 32, where the partial round trip is cheaper than the streaming it
-  // spreads (measured: at M = 64 / 128 one unit per W tile is faster)
+  // for M <= 32 or long K loops, where the partial round trip is cheaper than the
+  // streaming it spreads (measured: q_proj at M = 64 / 128 is faster unsplit)
   const int sms = cfg.max_ctas > 0 ? cfg.max_ctas : sm_count();
-  int splits = a.M <= 32 ? sms / p.num_nt : 1;
+  int splits = (a.M <= 32 || S >= 64) ? sms / p.num_nt : 1;
   static const int env_splits = [] { const char* e = getenv("MM_GEMM_SPLITS"); return e ? atoi(e) : 0; }();
   if (env_splits > 0) splits = env_splits;
   if (splits > S / 2) splits = S / 2;
