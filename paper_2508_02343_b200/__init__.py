@@ -19,7 +19,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmicromix_b200.so")
+LIB_PATH = os.environ.get("MM_LIB_PATH") or os.path.join(_HERE, "libmicromix_b200.so")   # override: tuning A/B builds
 
 MM_E2M1, MM_E3M2, MM_E2M3, MM_E4M3, MM_E5M2 = range(5)
 MM_SCALE_OCP, MM_SCALE_PAPER_EQ1 = 0, 1

@@ -21,7 +21,6 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
-#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -40,16 +39,9 @@ constexpr int kThreads2 = 256;
 __device__ unsigned long long g_trace[160][16];
 constexpr int A_BYTES = 128 * 128;       // this CTA's 128 rows x 128 B
 constexpr int B_BYTES = 128 * 128;       // this CTA's 128 W rows x 128 B
-// Scale factors travel in GROUPS of up to GS consecutive stages of one segment: one
-// TMA per operand row group brings the atoms of all GS stages (measured: per-stage
-// 512-B scale loads cost ~12 % of the all-FP8 mainloop).  A group buffer holds SFA
-// (GS x up to 2 atoms) and SFB (2 row groups x GS x up to 2 atoms); NSF buffers
-// rotate, each freed by a commit after the MMAs of its group's last stage.
-constexpr int GS = 3;
-constexpr int NSF = 2;
-constexpr int SFG_A = GS * 2 * 512;              // 3 KB
-constexpr int SFG_BYTES = SFG_A + 2 * SFG_A;     // 9 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SFA_BYTES = 2 * 512;       // up to 2 atoms (FP4 stage)
+constexpr int SFB_BYTES = 2 * 2 * 512;   // 2 row groups (N = 256) x up to 2 atoms
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
 constexpr int SF_STRIDE = 24;            // TMEM columns per scale slot: SFA 2x4, SFB 2x2x4
 // TMEM (512 columns): two 256-column accumulators that OVERLAP by 48 columns,
 // acc0 = [0, 256), acc1 = [208, 464), and two scale slots in [464, 512).  The
@@ -58,10 +50,7 @@ constexpr int SF_STRIDE = 24;            // TMEM columns per scale slot: SFA 2x4
 // the epilogue instead of after all of it.
 constexpr int ACC1_COL = 208;
 constexpr int SF_COL = 464;
-// epilogue staging: 4 warps x EPI_NBUF buffers x (32 x 32 BF16); one buffer per warp
-// when 6 operand stages take the shared memory
-template <int STAGES> __host__ __device__ constexpr int epi_nbuf() { return STAGES >= 6 ? 1 : 2; }
-template <int STAGES> __host__ __device__ constexpr int epi_bytes() { return 4 * epi_nbuf<STAGES>() * 32 * 64; }
+constexpr int EPI_BYTES = 4 * 2 * 32 * 64;  // epilogue staging: 4 warps x 2 buffers x (32 x 32 BF16)
 
 // Output tensor maps.  NP = 1: Y.  NP = kMaxPeers (NEXT F1, fused all-gather
 // epilogue): one map per rank of the peer window, each viewing THIS rank's column
@@ -74,9 +63,7 @@ struct YMaps {
 
 struct Gemm2Dev {
   int64_t M, N;
-  int num_m2, num_n, num_tiles;   // pair tiles of 256 x 256 (num_tiles counts cluster tiles)
-  int num_nc;                     // cluster tile columns: ceil(num_n / CP)
-  int raster_g;                   // pair-row blocks per raster group (tile_coords)
+  int num_m2, num_n, num_tiles;   // pair tiles of 256 x 256
   int nst0, nst1, nst2;           // stages per segment
   int n0, n1, n2;                 // real channels per segment
   int kp0, kp1, kp2;              // stored channels per segment
@@ -93,8 +80,8 @@ struct Gemm2Dev {
 // Tile raster: groups of up to 8 pair-row blocks (2048 rows of A) sweep all of N
 // before moving on, so a wave of tiles reuses the same A rows from L2 (for large M
 // the whole A does not fit in L2, W of one layer does).
-__device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& mb2, int& nb, int rg) {
-  const int G = num_m2 < rg ? num_m2 : rg;
+__device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& mb2, int& nb) {
+  const int G = num_m2 < 8 ? num_m2 : 8;
   const int per_group = G * num_n;
   const int grp = t / per_group, r = t - grp * per_group;
   const int rows = min(G, num_m2 - grp * G);
@@ -144,15 +131,8 @@ __device__ __forceinline__ void seg_stage(const Gemm2Dev& p, int j, int& kcoord,
   }
 }
 
-// CP = CTA pairs per cluster.  CP = 2: a cluster of 4 CTAs computes the pair tiles
-// (mb2, 2c) and (mb2, 2c + 1), which read the same 256 rows of A; each CTA loads
-// half of its 128-row A box and MULTICASTS it to the CTA with the same role in the
-// other pair, so L2 -> SM operand traffic per stage drops from 32 KB to 24 KB per
-// CTA.  Every CTA's smem stage is then written by two producers, so a stage is free
-// only when BOTH pairs' MMAs have consumed it: the empty barriers count CP commits,
-// and each leader's per-stage commit is multicast to all 2 * CP CTAs.
-template <int STAGES, int CP, int NP>
-__global__ void __launch_bounds__(kThreads2, 1)
+template <int STAGES, int NP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                 const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb0,
                 const __grid_constant__ CUtensorMap tb1, const __grid_constant__ CUtensorMap tb2,
@@ -164,28 +144,22 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * A_BYTES;
-  uint8_t* sSF = sB + STAGES * B_BYTES;            // [NSF][SFA | SFB rg0 | SFB rg1]
-  uint8_t* sEpi = sSF + NSF * SFG_BYTES;          // [4 warps][2][32 rows x 64 B] BF16 staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + epi_bytes<STAGES>());
+  uint8_t* sSFA = sB + STAGES * B_BYTES;
+  uint8_t* sSFB = sSFA + STAGES * SFA_BYTES;
+  uint8_t* sEpi = sSFB + STAGES * SFB_BYTES;      // [4 warps][2][32 rows x 64 B] BF16 staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_BYTES);
   uint64_t* full = bars;                  // [STAGES]  (used in the even CTA)
   uint64_t* empty = bars + STAGES;        // [STAGES]  (each CTA)
   uint64_t* tfull = bars + 2 * STAGES;    // [2] per accumulator (each CTA)
   uint64_t* tempty = tfull + 2;           // [2] accumulator fully drained (even CTA)
   uint64_t* tovl = tempty + 2;            // [2] overlap columns drained (even CTA)
-  uint64_t* sfempty = tovl + 2;           // [NSF] scale group buffer consumed (each CTA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfempty + NSF);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tovl + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t crank = ptx::cluster_ctarank();
-  const uint32_t rank = crank & 1;                 // role in the pair: 0 = MMA leader
-  const int pp = (int)(crank >> 1);                // pair inside the cluster (CP = 2)
-  const uint32_t leader = crank & ~1u;             // cluster rank of this pair's leader
-  constexpr uint16_t kAllMask = CP == 2 ? 0xF : 0x3;
-  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pp));
+  const uint32_t rank = ptx::cluster_ctarank();    // 0 = MMA leader
   const uint64_t t_start = ptx::globaltimer_ns();
   const bool trace = (p.dbg & 32) && lane == 0;
-  // scheduling unit: the cluster (one pair for CP = 1)
-  const int pair = blockIdx.x / (2 * CP), npairs = gridDim.x / (2 * CP);
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&ta0); ptx::tma_prefetch_desc(&ta1); ptx::tma_prefetch_desc(&ta2);
@@ -196,14 +170,13 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
       ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&empty[i]), CP);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(ptx::smem_u32(&tfull[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&tempty[i]), 8);   // 4 epilogue warps x 2 CTAs
       ptx::mbar_init(ptx::smem_u32(&tovl[i]), 8);
     }
-    for (int i = 0; i < NSF; ++i) ptx::mbar_init(ptx::smem_u32(&sfempty[i]), 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), 512);
@@ -224,14 +197,12 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t gidx = 0;   // scale groups started so far
       const uint32_t full0 = ptx::smem_u32(&full[0]);
       for (int it = 0; it < n_items; ++it) {
         int t, s0, s1;
         work_item(p, pair, npairs, S, it, t, s0, s1);
         int mb2, nb;
-        tile_coords(t, num_m2, p.num_nc, mb2, nb, p.raster_g);
-        nb = nb * CP + pp;
+        tile_coords(t, num_m2, p.num_n, mb2, nb);
         const int m0 = mb2 * 256 + 128 * (int)rank;      // this CTA's A rows
         const int n0 = nb * 256 + 128 * (int)rank;       // this CTA's W rows (its half of N)
         const int mgrp = mb2 * 2 + (int)rank;           // 128-row scale group of A
@@ -243,11 +214,11 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
           const CUtensorMap* tb = g == 0 ? &tb0 : (g == 1 ? &tb1 : &tb2);
           const CUtensorMap* tsa = g == 0 ? &tsa0 : (g == 1 ? &tsa1 : &tsa2);
           const CUtensorMap* tsb = g == 0 ? &tsb0 : (g == 1 ? &tsb1 : &tsb2);
-          const int box_atoms = (g == 0 ? 2 : 1) * GS;   // one scale group
+          const int box_atoms = g == 0 ? 2 : 1;
           // TMA counts GLOBAL element bits: a 16U6 (FP6) box of 128 elements lands
           // as 128 B per smem row but completes 96 B per row.
           const uint32_t ab = g == 1 ? (A_BYTES + B_BYTES) / 4 * 3 : (A_BYTES + B_BYTES);
-          const uint32_t sf_bytes = 3u * box_atoms * 512u;
+          const uint32_t cta_bytes = ab + 3u * box_atoms * 512u;
           const int sbase = g == 0 ? 0 : (g == 1 ? p.nst0 : p.nst0 + p.nst1);
           const int j_lo = max(s0 - sbase, 0), j_hi = min(s1 - sbase, nst);
           for (int j = j_lo; j < j_hi; ++j) {
@@ -263,27 +234,16 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
               continue;
             }
-            const bool gstart = (j == j_lo) || (j % GS == 0);
-            const bool load_sf = gstart && !no_sf;
-            if (gstart) {   // the group buffer this group fills must be free
-              ptx::mbar_wait(ptx::smem_u32(&sfempty[gidx & 1]), ((gidx >> 1) & 1) ^ 1, 26, (int)gidx, t);
-            }
-            if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * (load_sf ? ab + sf_bytes : ab));
-            if constexpr (CP == 1) {
-              ptx::tma_load_2d_cg2(ptx::smem_u32(sA + stage * A_BYTES), ta, fb, kcoord, m0);
-            } else {   // my half (64 rows) of the A box, to me and my counterpart in the other pair
-              ptx::tma_load_2d_cg2_mc(ptx::smem_u32(sA + stage * A_BYTES + pp * (A_BYTES / 2)), ta, fb, kcoord,
-                                      m0 + 64 * pp, (uint16_t)((1u << rank) | (1u << (rank + 2))));
-            }
+            if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * (no_sf ? ab : cta_bytes));
+            ptx::tma_load_2d_cg2(ptx::smem_u32(sA + stage * A_BYTES), ta, fb, kcoord, m0);
             ptx::tma_load_2d_cg2(ptx::smem_u32(sB + stage * B_BYTES), tb, fb, kcoord, n0);
-            if (load_sf) {
-              uint8_t* gbuf = sSF + (gidx & 1) * SFG_BYTES;
-              ptx::tma_load_2d_cg2(ptx::smem_u32(gbuf), tsa, fb, 0, mgrp * kp128 + atom0);
+            if (!no_sf) {
+              ptx::tma_load_2d_cg2(ptx::smem_u32(sSFA + stage * SFA_BYTES), tsa, fb, 0, mgrp * kp128 + atom0);
 #pragma unroll
               for (int rg = 0; rg < 2; ++rg)
-                ptx::tma_load_2d_cg2(ptx::smem_u32(gbuf + SFG_A * (1 + rg)), tsb, fb, 0, (nb * 2 + rg) * kp128 + atom0);
+                ptx::tma_load_2d_cg2(ptx::smem_u32(sSFB + stage * SFB_BYTES + rg * 1024), tsb, fb, 0,
+                                     (nb * 2 + rg) * kp128 + atom0);
             }
-            if (j == j_hi - 1 || j % GS == GS - 1) ++gidx;   // group ends
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }
@@ -299,9 +259,8 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      uint32_t gidx = 0;
       const uint32_t sA0 = ptx::smem_u32(sA), sB0 = ptx::smem_u32(sB);
-      const uint32_t sSF0 = ptx::smem_u32(sSF);
+      const uint32_t sSFA0 = ptx::smem_u32(sSFA), sSFB0 = ptx::smem_u32(sSFB);
       const uint32_t empty0 = ptx::smem_u32(&empty[0]), full0 = ptx::smem_u32(&full[0]);
       const bool no_mma = (p.dbg & 2) != 0;
       for (; it < n_items; ++it) {
@@ -333,18 +292,13 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
             const uint32_t sfb_t = sfa_t + 8;
             const uint64_t ad = ptx::smem_desc(sA0 + stage * A_BYTES, 16, 1024, 2);
             const uint64_t bd = ptx::smem_desc(sB0 + stage * B_BYTES, 16, 1024, 2);
-            // this stage's atoms inside its scale group buffer
-            const int jg = max(j_lo, j - j % GS);
-            const uint32_t sfo = sSF0 + (gidx & 1) * SFG_BYTES + (uint32_t)(j - jg) * (g == 0 ? 1024u : 512u);
-            const uint64_t sda = ptx::smem_desc(sfo, 0, 128, 0);
-            const uint64_t sdb0 = ptx::smem_desc(sfo + SFG_A, 0, 128, 0);
-            const uint64_t sdb1 = ptx::smem_desc(sfo + 2 * SFG_A, 0, 128, 0);
+            const uint64_t sda = ptx::smem_desc(sSFA0 + stage * SFA_BYTES, 0, 128, 0);
+            const uint64_t sdb0 = ptx::smem_desc(sSFB0 + stage * SFB_BYTES, 0, 128, 0);
+            const uint64_t sdb1 = ptx::smem_desc(sSFB0 + stage * SFB_BYTES + 1024, 0, 128, 0);
             if (nmma == 4 && !no_mma) {
-              if (g == 0)
-                ptx::stage_f4_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage, kAllMask);
-              else
-                ptx::stage_f8f6_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage,
-                                    (p.dbg & 64) ? 0u : 1u, kAllMask);
+              if (g == 0) ptx::stage_f4_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage);
+              else ptx::stage_f8f6_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage,
+                                       (p.dbg & 64) ? 0u : 1u);
               accum = 1;
             } else {
               // partial stage: scale copies for the atoms it uses, then nmma MMAs
@@ -366,20 +320,15 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
                   }
                   accum = 1;
                 }
-                ptx::tc_commit_cg2_mc(empty0 + 8 * stage, kAllMask);
+                ptx::tc_commit_cg2_mc(empty0 + 8 * stage, 0x3);
               }
               accum = __shfl_sync(0xffffffffu, accum, 0);
-              __syncwarp();
-            }
-            if (j == j_hi - 1 || j % GS == GS - 1) {   // group ends: free its scale buffer
-              ptx::commit_cg2_mc_elect(ptx::smem_u32(&sfempty[gidx & 1]), pair_mask);
-              ++gidx;
               __syncwarp();
             }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }
-        ptx::commit_cg2_mc_elect(ptx::smem_u32(&tfull[acc]), pair_mask);
+        ptx::commit_cg2_mc_elect(ptx::smem_u32(&tfull[acc]));
         if (trace && it < 3) g_trace[blockIdx.x][4 + 2 * it] = ptx::globaltimer_ns();
         if (trace && it == 0) g_trace[blockIdx.x][14] = clock64();
         __syncwarp();
@@ -393,18 +342,15 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     // chunk's conversion overlap the previous store; the accumulator is released to
     // the MMA warp as soon as its last chunk is in registers.
     const int q = warp & 3;                           // TMEM lane quadrant
-    const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(&tempty[0]), leader);
-    const uint32_t tovl_leader = ptx::mapa(ptx::smem_u32(&tovl[0]), leader);
-    constexpr int NB = epi_nbuf<STAGES>();
-    uint8_t* stg = sEpi + q * NB * 2048;
+    const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
+    const uint32_t tovl_leader = ptx::mapa(ptx::smem_u32(&tovl[0]), 0);
+    uint8_t* stg = sEpi + q * 2 * 2048;
     int nstore = 0;
     for (int it = 0; it < n_items; ++it) {
       int t, s0, s1;
       work_item(p, pair, npairs, S, it, t, s0, s1);
       int mb2, nb;
-      tile_coords(t, num_m2, p.num_nc, mb2, nb, p.raster_g);
-      nb = nb * CP + pp;
-      const bool dead = nb >= p.num_n;   // CP = 2 with odd num_n: the second pair's tile is past N
+      tile_coords(t, num_m2, p.num_n, mb2, nb);
       // stream-K roles of this item: leave a partial (head of a tile) / add one (tail)
       const bool to_ws = s1 < S, from_ws = s0 > 0;
       const int wrow = 128 * (int)rank + q * 32 + lane;   // row inside the 256-row pair tile
@@ -452,7 +398,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
             if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
           }
         }
-        if ((p.dbg & 4) || dead) continue;
+        if (p.dbg & 4) continue;
         if (to_ws) {   // fp32 partial -> workspace row (128 B per chunk per thread)
           float4* dst = reinterpret_cast<float4*>(p.ws + ((size_t)pair * 256 + wrow) * 256 + 32 * c);
 #pragma unroll
@@ -475,8 +421,8 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         uint32_t w[16];
 #pragma unroll
         for (int v = 0; v < 16; ++v) w[v] = ptx::pack_bf16x2(__uint_as_float(r[2 * v]), __uint_as_float(r[2 * v + 1]));
-        uint8_t* buf = stg + (nstore % NB) * 2048;
-        if (lane == 0) ptx::bulk_wait_group_read<NB - 1>();   // the store that last used `buf` has read it
+        uint8_t* buf = stg + (nstore & 1) * 2048;
+        if (lane == 0) ptx::bulk_wait_group_read<1>();   // the store that last used `buf` has read it
         __syncwarp();
         // row `lane` = 64 B in the TMA 64-byte swizzle layout (16-byte chunk k of row
         // r at chunk k ^ ((r >> 1) & 3)): conflict-free, and w[] is indexed statically
@@ -562,15 +508,15 @@ bool stream_k_workspace(cudaStream_t s, int npairs, float** ws, int** flags) {
   return true;
 }
 
-template <int STAGES, int CP, int NP>
+template <int STAGES, int NP>
 cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches, const char** err) {
   CUtensorMap maps[12];
   YMaps<NP> ym;
   int first = -1;
   for (int g = 0; g < 3; ++g) {
     if (a.geom.n[g] == 0) continue;
-    const int box_atoms = (g == 0 ? 2 : 1) * GS;   // one scale group per load
-    if (!make_operand_map(&maps[g], a.a_codes[g], g, a.geom.kp[g], a.M, a.geom.pitch[g], 128 / CP) ||
+    const int box_atoms = g == 0 ? 2 : 1;
+    if (!make_operand_map(&maps[g], a.a_codes[g], g, a.geom.kp[g], a.M, a.geom.pitch[g], 128) ||
         !make_operand_map(&maps[3 + g], a.w_codes[g], g, a.geom.kp[g], a.N, a.geom.pitch[g], 128) ||
         !make_sf_map(&maps[6 + g], a.a_sf[g], a.M, a.geom.kp[g], box_atoms) ||
         !make_sf_map(&maps[9 + g], a.w_sf[g], a.N, a.geom.kp[g], box_atoms)) {
@@ -606,9 +552,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.N = a.N;
   p.num_m2 = (int)((a.M + 255) / 256);
   p.num_n = (int)((a.N + 255) / 256);
-  p.num_nc = (p.num_n + CP - 1) / CP;
-  p.num_tiles = p.num_m2 * p.num_nc;
-  { const char* e = getenv("MM_GEMM_RASTER_G"); p.raster_g = e ? atoi(e) : 8; if (p.raster_g < 1) p.raster_g = 1; }
+  p.num_tiles = p.num_m2 * p.num_n;
   p.nst0 = (a.geom.kp[0] + 255) / 256;
   p.nst1 = a.geom.kp[1] / 128;
   p.nst2 = a.geom.kp[2] / 128;
@@ -622,20 +566,17 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.ndst = ndst;
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   if (p.num_tiles == 0) return cudaSuccess;
-  int grid = sm_count() / (2 * CP) * (2 * CP);
-  if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas / (2 * CP) * (2 * CP);
-  if (grid < 2 * CP) grid = 2 * CP;
-  if (grid > 2 * CP * p.num_tiles) grid = 2 * CP * p.num_tiles;
-  static const bool nonpersist = [] { const char* e = getenv("MM_GEMM_NONPERSIST"); return e && atoi(e); }();
-  if (nonpersist) grid = 2 * CP * p.num_tiles;   // experiment: one tile per pair, hardware scheduling
+  int grid = sm_count() & ~1;
+  if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas & ~1;
+  if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
   // Stream-K when the last wave of tiles would be ragged and there are only a few
   // waves (each pair then finishes at most one tile left by its neighbour).
-  const int npairs = grid / 2;   // (stream-K: CP = 1 only)
+  const int npairs = grid / 2;
   // Opt-in (MM_GEMM_STREAMK=1): measured on q_proj it LOSES (40.9 vs 29.6 us) -- each
   // extra work item costs a full TMEM drain plus a 256 KB fp32 partial round trip,
   // more than the ragged wave it removes.  Kept as a tested alternative schedule.
   const bool sk_env_on = [] { const char* e = getenv("MM_GEMM_STREAMK"); return e && atoi(e) == 1; }();
-  p.stream_k = (CP == 1 && sk_env_on && !cfg.no_stream_k && p.num_tiles > npairs && p.num_tiles % npairs != 0 &&
+  p.stream_k = (sk_env_on && !cfg.no_stream_k && p.num_tiles > npairs && p.num_tiles % npairs != 0 &&
                 p.num_tiles < 4 * npairs) ? 1 : 0;
   if (p.stream_k) {
     if (!stream_k_workspace(s, npairs, &p.ws, &p.ws_flag)) {
@@ -643,29 +584,11 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
       return cudaErrorMemoryAllocation;
     }
   }
-  const size_t smem =
-      1024 + (size_t)STAGES * STAGE_BYTES + NSF * SFG_BYTES + epi_bytes<STAGES>() + (2 * STAGES + 6 + NSF) * 8 + 16;
-  auto kern = mixgemm2_kernel<STAGES, CP, NP>;
+  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + EPI_BYTES + (2 * STAGES + 6) * 8 + 16;
+  auto kern = mixgemm2_kernel<STAGES, NP>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
-  if (p.dbg & 128) {   // diagnostics: co-resident clusters of this configuration
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(kThreads2);
-    lc.dynamicSmemBytes = smem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2 * CP;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    int ncl = -1;
-    cudaError_t oe = cudaOccupancyMaxActiveClusters(&ncl, kern, &lc);
-    fprintf(stderr, "[mm gemm2] CP=%d grid=%d smem=%zu max active clusters=%d (%s)\n", CP, grid, smem, ncl,
-            cudaGetErrorString(oe));
-  }
-  e = launch_pdl_cluster(kern, dim3(grid), dim3(kThreads2), smem, s, 2 * CP, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
+  e = launch_pdl(kern, dim3(grid), dim3(kThreads2), smem, s, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
                  maps[6], maps[7], maps[8], maps[9], maps[10], maps[11], ym, p);
   if (launches) ++*launches;
   return e != cudaSuccess ? e : cudaGetLastError();
@@ -683,26 +606,9 @@ namespace mmx {
 
 cudaError_t launch_mixed_gemm_2cta(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
                                    const char** err) {
-  // Pairs per cluster: 2 (A multicast across two pair tiles) unless MM_GEMM_CP=1.
-  // CP = 2 needs an even pair-tile column count unless forced by MM_GEMM_CP=2 (an odd
-  // count leaves the second pair of the last cluster column computing a tile past N).
-  static const int cp_env = [] { const char* e = getenv("MM_GEMM_CP"); return e ? atoi(e) : 0; }();
-  const int64_t num_n = (a.N + 255) / 256;
-  int c = cfg.cluster_pairs ? cfg.cluster_pairs : cp_env;
-  // Measured: no faster per tile at q_proj and only 33 clusters of 4 are co-resident
-  // (132 SMs), so the default stays 1 (CP = 2 is kept, tested, opt-in).
-  if (c == 0) c = 1;
-  if (c == 2 && num_n % 2 && cp_env != 2) c = 1;
-  static const int st_env = [] { const char* e = getenv("MM_GEMM_STAGES"); return e ? atoi(e) : 0; }();
-  const int st = cfg.num_stages ? cfg.num_stages : (st_env ? st_env : 5);
-  if (a.n_dst > 0) return run2<5, 1, kMaxPeers>(a, cfg, s, launches, err);   // fused all-gather epilogue
-  if (c == 1) {
-    if (st == 4) return run2<4, 1, 1>(a, cfg, s, launches, err);
-    if (st == 6) return run2<6, 1, 1>(a, cfg, s, launches, err);
-    return run2<5, 1, 1>(a, cfg, s, launches, err);
-  }
-  if (cfg.num_stages == 4) return run2<4, 2, 1>(a, cfg, s, launches, err);
-  return run2<5, 2, 1>(a, cfg, s, launches, err);
+  if (a.n_dst > 0) return run2<5, kMaxPeers>(a, cfg, s, launches, err);   // fused all-gather epilogue
+  if (cfg.num_stages == 4) return run2<4, 1>(a, cfg, s, launches, err);
+  return run2<5, 1>(a, cfg, s, launches, err);
 }
 
 }  // namespace mmx
