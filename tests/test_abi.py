@@ -106,3 +106,29 @@ def test_plan_diagnostics_host(L):
     assert [round(v * K) for v in d.p] == list(cal["n"])
     pitch = [(n + 127) // 128 * 128 * b // 8 for n, b in zip(cal["n"], (4, 6, 8))]
     assert d.stored_bytes_per_row == sum(pitch) + sum((n + 127) // 128 * 4 for n in cal["n"])
+
+
+def test_peer_window_host_queries_and_validation(L):
+    """Fused all-gather epilogue (NEXT F1): buffer size, handle size and the window
+    argument checks are host logic."""
+    # [Y: BF16 M x ldy padded to 256 B][64 x u32 flags]
+    assert L.mm_peer_buffer_bytes(3, 8) == 256 + 256
+    assert L.mm_peer_buffer_bytes(2048, 8192) == 2048 * 8192 * 2 + 256
+    assert L.mm_ipc_handle_bytes() == 72            # cudaIpcMemHandle_t + u64 offset
+    h = ctypes.c_void_p()
+    bufs = (ctypes.c_void_p * 9)(*([256] * 9))
+    assert L.mm_peer_window_from_ptrs(0, 9, bufs, 16, 64, ctypes.byref(h)) == 1      # world > 8
+    assert L.mm_peer_window_from_ptrs(3, 2, bufs, 16, 64, ctypes.byref(h)) == 1      # rank >= world
+    assert L.mm_peer_window_from_ptrs(0, 2, bufs, 16, 60, ctypes.byref(h)) == 2      # ldy % 8
+    odd = (ctypes.c_void_p * 2)(256, 257)
+    assert L.mm_peer_window_from_ptrs(0, 2, odd, 16, 64, ctypes.byref(h)) == 3       # alignment
+    assert L.mm_peer_window_from_ptrs(1, 2, bufs, 16, 64, ctypes.byref(h)) == 0
+    assert L.mm_peer_window_close(h) == 0
+    assert L.mm_peer_window_close(None) == 0
+
+
+def test_gemm_config_values(L):
+    for bn in (0, 1, 128, 256, 512):
+        assert L.mm_set_gemm_config(bn, 0, 0) == 0
+    assert L.mm_set_gemm_config(64, 0, 0) == 1
+    assert L.mm_set_gemm_config(0, 0, 0) == 0
