@@ -36,7 +36,7 @@ constexpr int kThreads2 = 256;
 // Timeline trace (env MM_GEMM_DEBUG & 32; read with mm_debug_gemm_trace): per CTA
 // [start, setup, first stage ready, tile0 start, tile0 issued, tile1 start, tile1
 // issued, tile2 start, tile2 issued, epi0 ready, epi1 ready, epi2 ready, epi done].
-__device__ unsigned long long g_trace[160][16];
+__device__ unsigned long long g_trace[160][24];
 constexpr int A_BYTES = 128 * 128;       // this CTA's 128 rows x 128 B
 constexpr int B_BYTES = 128 * 128;       // this CTA's 128 W rows x 128 B
 constexpr int SFA_BYTES = 2 * 512;       // up to 2 atoms (FP4 stage)
@@ -269,9 +269,11 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         const int acc = it & 1;
         const uint32_t d_t = tmem_base + (acc ? ACC1_COL : 0);
         ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), ((it >> 1) & 1) ^ 1, 22, it, t);   // tile it-2 drained acc
+        if (trace && it == 1) g_trace[blockIdx.x][16] = ptx::globaltimer_ns();
         if (it > 0) ptx::mbar_wait(ptx::smem_u32(&tovl[acc ^ 1]), ((it - 1) >> 1) & 1, 25, it, t);  // overlap of it-1
         if (trace && it < 3) g_trace[blockIdx.x][3 + 2 * it] = ptx::globaltimer_ns();
         if (trace && it == 0) g_trace[blockIdx.x][13] = clock64();
+        if (trace && it == 1) g_trace[blockIdx.x][22] = clock64();
         ptx::tc_fence_after();
         uint32_t accum = 0;
 #pragma unroll
@@ -365,6 +367,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       const int acc = it & 1;
       ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), (it >> 1) & 1, 24, it, t);
       if (trace && q == 0 && it < 3) g_trace[blockIdx.x][9 + it] = ptx::globaltimer_ns();
+      if (trace && q == 0 && it == 0 && rank == 0) g_trace[blockIdx.x][21] = clock64();
       ptx::tc_fence_after();
       const int row0 = mb2 * 256 + 128 * (int)rank + q * 32;
       const int n0 = nb * 256;
@@ -380,12 +383,15 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         const int c = acc ? i : (i + 6) & 7;
         uint32_t r[32];
         if (i == 0) {
+          if (trace && q == 0 && it == 0 && rank == 0) g_trace[blockIdx.x][19] = clock64();
           ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
           ptx::tmem_ld_32x32b_x32(trow + 32 * (acc ? 1 : 7), rn);
           ptx::tc_wait_ld();
+          if (trace && q == 0 && it == 0 && rank == 0) g_trace[blockIdx.x][20] = clock64();
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_cluster(tovl_leader + 8 * acc);   // overlap drained
+          if (trace && q == 0 && it == 0) g_trace[blockIdx.x][17 + (int)rank] = ptx::globaltimer_ns();
         } else if (i == 1) {
 #pragma unroll
           for (int v = 0; v < 32; ++v) r[v] = rn[v];
@@ -599,7 +605,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
 
 // Debug hook (not part of include/mm.h): copy the GEMM timeline trace to the host.
 extern "C" int mm_debug_gemm_trace(unsigned long long* h, int n) {
-  return (int)cudaMemcpyFromSymbol(h, mmx::g_trace, sizeof(unsigned long long) * (size_t)(n < 2560 ? n : 2560));
+  return (int)cudaMemcpyFromSymbol(h, mmx::g_trace, sizeof(unsigned long long) * (size_t)(n < 3840 ? n : 3840));
 }
 
 namespace mmx {
