@@ -211,7 +211,9 @@ def test_stream_k_matches_oracle_and_data_parallel(M, N, n, monkeypatch):
 # ---- small-M path (NEXT F3): swap-AB + split-K kernel (gemm_sm.cu) ----------------
 @pytest.mark.parametrize("M,N,n", [(1, 256, (128, 64, 64)), (7, 384, (256, 128, 128)), (16, 4096, (2240, 1184, 672)),
                                    (33, 1000 - 1000 % 16, (512, 256, 256)), (64, 2048, (96, 160, 224)),
-                                   (100, 4096, (2240, 1184, 672)), (128, 1536, (1024, 512, 256))])
+                                   (100, 4096, (2240, 1184, 672)), (128, 1536, (1024, 512, 256)),
+                                   (16, 512, (0, 0, 1024)), (8, 256, (2048, 0, 0)), (24, 2048, (0, 512, 0)),
+                                   (32, 4096, (8512, 3840, 1984))])
 def test_small_m_swap_ab_split_k(M, N, n):
     """The swap-AB / split-K kernel (forced through block_n = 1; automatic for M <= 32),
     ragged rows and 128-channel tiles, every segment mix, 1..4 K splits."""

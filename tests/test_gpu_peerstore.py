@@ -53,7 +53,8 @@ def _virtual_ranks(plan, a, shards, M, Ns, G, ldy, iters=2):
 
 
 @pytest.mark.parametrize("M,Ns,G,n", [(300, 256, 2, (256, 128, 128)), (256, 144, 4, (2240, 1184, 672)),
-                                      (520, 512, 8, (512, 256, 256)), (64, 96, 2, (128, 64, 64))])
+                                      (520, 512, 8, (512, 256, 256)), (64, 96, 2, (128, 64, 64)),
+                                      (2048, 512, 8, (2240, 1184, 672)), (130, 272, 3, (0, 256, 0))])
 def test_peerstore_virtual_ranks_equal_1gpu(M, Ns, G, n):
     plan, a, shards, y_ref = _setup(M, Ns, G, n)
     N = Ns * G
