@@ -30,6 +30,9 @@ namespace {
 constexpr int kThreadsSm = 256;
 constexpr int W_BYTES = 128 * 128;   // 128 W rows x 128 B per stage
 constexpr int kMaxSplits = 4;
+// Timeline trace (env MM_GEMM_DEBUG & 32; mm_debug_gemm_sm_trace): per CTA
+// [start, setup done, first stage full, last stage full, MMAs done (tfull), partial written, end].
+__device__ unsigned long long g_sm_trace[1024][8];
 
 struct SmDev {
   int64_t M, N;
@@ -44,6 +47,7 @@ struct SmDev {
   int64_t ldy;
   float* ws;             // [num_nt * splits][BNM][128] FP32 partials (splits > 1)
   int* cnt;              // [num_nt] arrival counters (left at zero)
+  int dbg;
 };
 
 template <int BNM, int STAGES>
@@ -101,6 +105,8 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
   __shared__ int s_last;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const bool trace = (p.dbg & 32) && blockIdx.x < 1024;
+  if (trace && threadIdx.x == 0) g_sm_trace[blockIdx.x][0] = ptx::globaltimer_ns();
   const int nt = blockIdx.x / p.splits, ks = blockIdx.x % p.splits;
   const int S = p.nst[0] + p.nst[1] + p.nst[2];
   const int s_lo = (int)((int64_t)ks * S / p.splits), s_hi = (int)((int64_t)(ks + 1) * S / p.splits);
@@ -124,6 +130,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
   const uint32_t tmem_base = *tmem_slot;
   ptx::grid_dep_launch();
   ptx::grid_dep_wait();   // A and its scales may come from the preceding kernel
+  if (trace && threadIdx.x == 0) g_sm_trace[blockIdx.x][1] = ptx::globaltimer_ns();
 
   if (warp == 0) {
     // ============================ TMA producer ============================
@@ -154,6 +161,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
     for (int s = s_lo; s < s_hi; ++s) {
       const SmStage si = sm_stage(p, s);
       ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase, 32, s, nt);
+      if (trace && lane == 0 && (s == s_lo || s == s_hi - 1)) g_sm_trace[blockIdx.x][s == s_lo ? 2 : 3] = ptx::globaltimer_ns();
       ptx::tc_fence_after();
       if (lane == 0) {
         const uint32_t sfw_t = tmem_base + BNM + stage * C::SF_STRIDE;
@@ -190,6 +198,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
     const int64_t n = (int64_t)nt * 128 + nl;
     const bool empty_range = s_hi <= s_lo;              // (splits <= stages, never true)
     if (!empty_range) ptx::mbar_wait(ptx::smem_u32(tfull), 0, 33, nt, ks);
+    if (trace && q == 0 && lane == 0) g_sm_trace[blockIdx.x][4] = ptx::globaltimer_ns();
     ptx::tc_fence_after();
     const int M = (int)p.M;
     if (p.splits == 1) {
@@ -221,6 +230,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
         for (int j = 0; j < 32; ++j) __stcg(mine + (size_t)(32 * c + j) * 128 + nl, __uint_as_float(r[j]));
       }
       // 2) arrival: the last unit of this W tile reduces all partials in split order
+      if (trace && q == 0 && lane == 0) g_sm_trace[blockIdx.x][5] = ptx::globaltimer_ns();
       __threadfence();
       ptx::named_bar_sync(1, 128);
       if (warp == 4 && lane == 0) {
@@ -259,6 +269,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  if (trace && threadIdx.x == 0) g_sm_trace[blockIdx.x][6] = ptx::globaltimer_ns();
   if (warp == 2) ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
 }
 
@@ -322,6 +333,7 @@ cudaError_t run_sm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int
   }
   p.y = a.y;
   p.ldy = a.ldy;
+  { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   if (p.num_nt == 0 || a.M == 0) return cudaSuccess;
   // splits: fill the SMs once (one CTA per SM), at least 2 stages per unit; only
   // for M <= 32 or long K loops, where the partial round trip is cheaper than the
@@ -361,3 +373,8 @@ cudaError_t launch_mixed_gemm_smallm(const GemmArgs& a, const GemmConfig& cfg, c
 }
 
 }  // namespace mmx
+
+// Debug hook (not part of include/mm.h): copy the small-M GEMM trace to the host.
+extern "C" int mm_debug_gemm_sm_trace(unsigned long long* h, int n) {
+  return (int)cudaMemcpyFromSymbol(h, mmx::g_sm_trace, sizeof(unsigned long long) * (size_t)(n < 8192 ? n : 8192));
+}
