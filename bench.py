@@ -443,7 +443,7 @@ def run_gpu(args, rank, world, local):
                                f"(fp8 = 2x, fp4 = 4x)"},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": pmix, "unit": "TFLOP/s",
                      "frac": gemm_tflops / pmix, "traffic": None,
-                     "kernel": "mixgemm_kernel (algorithmic 2*M*N*K per launch; mix-weighted MXFP4/FP8 peak)"},
+                     "kernel": "mixgemm2_kernel (CTA-pair tcgen05; algorithmic 2*M*N*K per launch; mix-weighted MXFP4/FP8 peak)"},
         "rq_roofline": {"bound": "hbm", "achieved": rq_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                         "frac": rq_gbs / pk["hbm_gbs"], "traffic": None,
                         "kernel": "rq_kernel (algorithmic BF16 read + packed codes + scales)"},
