@@ -47,6 +47,7 @@ struct SmDev {
   int64_t ldy;
   float* ws;             // [num_nt * splits][BNM][128] FP32 partials (splits > 1)
   int* cnt;              // [num_nt] arrival counters (left at zero)
+  int interleave;        // 1: units take every splits-th stage, 0: contiguous K ranges (default; measured equal)
   int dbg;
 };
 
@@ -109,7 +110,13 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
   if (trace && threadIdx.x == 0) g_sm_trace[blockIdx.x][0] = ptx::globaltimer_ns();
   const int nt = blockIdx.x / p.splits, ks = blockIdx.x % p.splits;
   const int S = p.nst[0] + p.nst[1] + p.nst[2];
-  const int s_lo = (int)((int64_t)ks * S / p.splits), s_hi = (int)((int64_t)(ks + 1) * S / p.splits);
+  // Stages of this unit: interleaved (ks, ks + splits, ...) so that the splits of one
+  // W tile read neighbouring 128-byte pieces of the same rows at the same time (DRAM
+  // page locality), or one contiguous K range (p.interleave = 0).
+  const int s_step = p.interleave ? p.splits : 1;
+  const int s_lo = p.interleave ? ks : (int)((int64_t)ks * S / p.splits);
+  const int s_end = p.interleave ? S : (int)((int64_t)(ks + 1) * S / p.splits);
+  const int s_fin = s_end > s_lo ? s_lo + (s_end - 1 - s_lo) / s_step * s_step : s_lo - 1;   // last stage
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tw0); ptx::tma_prefetch_desc(&tw1); ptx::tma_prefetch_desc(&tw2);
@@ -139,7 +146,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
       const CUtensorMap* ta[3] = {&ta0, &ta1, &ta2};
       int stage = 0;
       uint32_t phase = 0;
-      for (int s = s_lo; s < s_hi; ++s) {
+      for (int s = s_lo; s < s_end; s += s_step) {
         const SmStage si = sm_stage(p, s);
         ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1, 31, s, nt);
         const uint32_t fb = ptx::smem_u32(&full[stage]);
@@ -158,10 +165,10 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
     // ============================ MMA issuer ============================
     int stage = 0;
     uint32_t phase = 0;
-    for (int s = s_lo; s < s_hi; ++s) {
+    for (int s = s_lo; s < s_end; s += s_step) {
       const SmStage si = sm_stage(p, s);
       ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase, 32, s, nt);
-      if (trace && lane == 0 && (s == s_lo || s == s_hi - 1)) g_sm_trace[blockIdx.x][s == s_lo ? 2 : 3] = ptx::globaltimer_ns();
+      if (trace && lane == 0 && (s == s_lo || s == s_fin)) g_sm_trace[blockIdx.x][s == s_lo ? 2 : 3] = ptx::globaltimer_ns();
       ptx::tc_fence_after();
       if (lane == 0) {
         const uint32_t sfw_t = tmem_base + BNM + stage * C::SF_STRIDE;
@@ -186,7 +193,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
           }
         }
         ptx::tc_commit(ptx::smem_u32(&empty[stage]));
-        if (s == s_hi - 1) ptx::tc_commit(ptx::smem_u32(tfull));
+        if (s == s_fin) ptx::tc_commit(ptx::smem_u32(tfull));
       }
       __syncwarp();
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -196,7 +203,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
     const int q = warp & 3;
     const int nl = q * 32 + lane;                       // row of the W tile
     const int64_t n = (int64_t)nt * 128 + nl;
-    const bool empty_range = s_hi <= s_lo;              // (splits <= stages, never true)
+    const bool empty_range = s_fin < s_lo;             // (splits <= stages / 2, never true)
     if (!empty_range) ptx::mbar_wait(ptx::smem_u32(tfull), 0, 33, nt, ks);
     if (trace && q == 0 && lane == 0) g_sm_trace[blockIdx.x][4] = ptx::globaltimer_ns();
     ptx::tc_fence_after();
@@ -334,6 +341,7 @@ cudaError_t run_sm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int
   p.y = a.y;
   p.ldy = a.ldy;
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
+  { const char* e = getenv("MM_GEMM_SPLIT_INTERLEAVE"); p.interleave = e ? atoi(e) : 0; }
   if (p.num_nt == 0 || a.M == 0) return cudaSuccess;
   // splits: fill the SMs once (one CTA per SM), at least 2 stages per unit; only
   // for M <= 32 or long K loops, where the partial round trip is cheaper than the
