@@ -192,7 +192,13 @@ mm_status mm_rmsnorm_reorder_quantize_act(const void* d_x, int64_t M, int64_t ld
 /* Mixed block-scaled GEMM (§3.2, Eq. 2): Y[M, N] = A W^T over the three
  * K-segments, one FP32 accumulator, BF16 round-to-nearest-even output
  * (row-major, ld = ldy >= N, ldy % 8 == 0).  A and W must come from `plan`
- * (fingerprints equal) -- else MM_ERR_PLAN_MISMATCH.  N % 16 == 0. */
+ * (fingerprints equal) -- else MM_ERR_PLAN_MISMATCH.  N % 16 == 0.
+ * Small M (<= 32, or <= 128 with a long K loop) runs the swap-AB / split-K kernel:
+ * each K split keeps its own FP32 accumulator and the partials are added in split
+ * order (deterministic; reading R28).  Its FP32 partials live in a
+ * library-owned workspace per (device, stream), allocated on the first such call
+ * and grown on demand (<= num_tiles x 4 splits x 64 KB; this is the one allocation a
+ * hot call can make, once). */
 mm_status mm_mixed_gemm_bf16(const mm_mx_tensor* a, const mm_mx_tensor* w,
                              const mm_plan* plan, void* d_y, int64_t ldy,
                              mm_stream_t stream);
