@@ -556,6 +556,9 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     ptx::mbar_wait(ptx::smem_u32(&full[s]), ph, 12, s, (int)i);
     if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][2 + 2 * i] = ptx::globaltimer_ns();
     // ---- in-place transpose: box [R rows][256] -> 256 slots of R values ----
+    // (NORM: the exact per-row sums of squares are accumulated from the same
+    // registers, so the norm needs no second pass over the stage.)
+    double nhi[4] = {0, 0, 0, 0}, nlo[4] = {0, 0, 0, 0};
     if constexpr (R > 1) {
       for (int b = gw; b < nbox && dbg < 2; b += group_warps) {
         uint8_t* box = st + b * 512 * R;
@@ -563,6 +566,18 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) w[rho] = *reinterpret_cast<const uint4*>(box + rho * 512 + lane * 16);
         __syncwarp();
+        if constexpr (NORM) {
+#pragma unroll
+          for (int rho = 0; rho < R; ++rho) {
+            const uint32_t* u = reinterpret_cast<const uint32_t*>(&w[rho]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const double x0 = bf16_f64(u[k] & 0xFFFFu), x1 = bf16_f64(u[k] >> 16);
+              dd_add(nhi[rho], nlo[rho], x0 * x0);
+              dd_add(nhi[rho], nlo[rho], x1 * x1);
+            }
+          }
+        }
         const uint32_t* u0 = reinterpret_cast<const uint32_t*>(&w[0]);
         const uint32_t* u1 = reinterpret_cast<const uint32_t*>(&w[1]);
         if constexpr (R == 2) {
@@ -592,8 +607,8 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       if constexpr (NORM) {
         const ST* slots = reinterpret_cast<const ST*>(st);
         // exact per-row sums of squares (double-double), group reduction in a fixed order
-        double hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
-        for (int pc = gw * 32 + lane; pc < K; pc += gthreads) {
+        double hi[4] = {nhi[0], nhi[1], nhi[2], nhi[3]}, lo[4] = {nlo[0], nlo[1], nlo[2], nlo[3]};
+        for (int pc = gw * 32 + lane; R == 1 && pc < K; pc += gthreads) {   // R > 1: summed in the transpose
           const ST v = slots[pc];
           { const double x = bf16_f64(slot_bits<0>(v)); dd_add(hi[0], lo[0], x * x); }
           if constexpr (R >= 2) { const double x = bf16_f64(slot_bits<1>(v)); dd_add(hi[1], lo[1], x * x); }

@@ -151,7 +151,7 @@ def test_errors_are_loud():
 
 
 @pytest.mark.parametrize("M,K,n,eps", [(16, 256, (128, 64, 64), 1e-5), (300, 4096, (2240, 1184, 672), 1e-6),
-                                       (77, 14336, (8512, 3840, 1984), 1e-5)])
+                                       (77, 14336, (8512, 3840, 1984), 1e-5), (131, 1120, (512, 320, 288), 1e-5)])
 def test_rmsnorm_fused_bit_exact(M, K, n, eps):
     """F2: RMSNorm fused into the RQ == the oracle's norm (reading R27) followed by the
     oracle's reorder-quantize, bit for bit (codes, scales, padding)."""
