@@ -403,14 +403,12 @@ cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStre
   if (a.n_dst > 0) bn = 512;   // the fused all-gather epilogue lives in the CTA-pair kernel
   // small M (decode-like): swap-AB + split-K kernel (gemm_sm.cu), unless a tile
   // configuration is forced or MM_GEMM_SMALLM=0
-  // Auto (measured, N = 4096: 10-13 us vs 25 us at M <= 32): few enough 128-row W
-  // tiles that every tile gets >= 2 K splits, and either M <= 32 or a long K loop
-  // (>= 64 stages, e.g. down_proj K = 14336) whose W streaming outweighs the split-K
-  // reduction of up to 128 rows; otherwise the 128 x 256 tile kernel is as fast.
-  // MM_GEMM_SMALLM=1 forces it for any M <= 128.
+  // Auto (measured, q_proj N = 4096: M = 1 / 32 / 64 / 128 -> 10 / 13 / 18 / 26 us vs
+  // 25-27 us with 128 x 256 tiles): every M <= 128 when few enough 128-row W tiles
+  // exist for each to get >= 2 K splits; otherwise the tile kernel.
+  // MM_GEMM_SMALLM=1 forces it for any M <= 128, =0 disables it.
   static const int smallm_env = [] { const char* e = getenv("MM_GEMM_SMALLM"); return e ? atoi(e) : -1; }();
-  const int kstages = (a.geom.kp[0] + 255) / 256 + a.geom.kp[1] / 128 + a.geom.kp[2] / 128;
-  const bool smallm_auto = (a.M <= 32 || (a.M <= 128 && kstages >= 64)) && 2 * ((a.N + 127) / 128) <= sm_count();
+  const bool smallm_auto = a.M <= 128 && 2 * ((a.N + 127) / 128) <= sm_count();
   if (a.n_dst == 0 && a.M <= 128 &&
       (cfg.block_n == 1 || (cfg.block_n == 0 && smallm_env != 0 && (smallm_env == 1 || smallm_auto))))
     return launch_mixed_gemm_smallm(a, cfg, s, launches, err);

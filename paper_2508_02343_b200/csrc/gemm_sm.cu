@@ -343,11 +343,10 @@ cudaError_t run_sm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   { const char* e = getenv("MM_GEMM_SPLIT_INTERLEAVE"); p.interleave = e ? atoi(e) : 0; }
   if (p.num_nt == 0 || a.M == 0) return cudaSuccess;
-  // splits: fill the SMs once (one CTA per SM), at least 2 stages per unit; only
-  // for M <= 32 or long K loops, where the partial round trip is cheaper than the
-  // streaming it spreads (measured: q_proj at M = 64 / 128 is faster unsplit)
+  // splits: fill the SMs once (one CTA per SM), at least 2 stages per unit, at most
+  // kMaxSplits (the last unit's reduction reads splits x M x 512 B per tile)
   const int sms = cfg.max_ctas > 0 ? cfg.max_ctas : sm_count();
-  int splits = (a.M <= 32 || S >= 64) ? sms / p.num_nt : 1;
+  int splits = sms / p.num_nt;
   static const int env_splits = [] { const char* e = getenv("MM_GEMM_SPLITS"); return e ? atoi(e) : 0; }();
   if (env_splits > 0) splits = env_splits;
   if (splits > S / 2) splits = S / 2;
