@@ -139,8 +139,11 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
   ptx::grid_dep_wait();   // A and its scales may come from the preceding kernel
   if (trace && threadIdx.x == 0) g_sm_trace[blockIdx.x][1] = ptx::globaltimer_ns();
 
-  if (warp == 0) {
-    // ============================ TMA producer ============================
+  if (warp == 0 || warp == 3) {
+    // ============================ TMA producers ============================
+    // warp 0: transaction count + W and A tiles; warp 3: the scale atoms (two issuing
+    // threads, as in the CTA-pair kernel).
+    const bool ops_w = warp == 0;
     if (lane == 0) {
       const CUtensorMap* tw[3] = {&tw0, &tw1, &tw2};
       const CUtensorMap* ta[3] = {&ta0, &ta1, &ta2};
@@ -152,12 +155,15 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
         const uint32_t fb = ptx::smem_u32(&full[stage]);
         const int kp128 = p.kp[si.g] / 128;
         const uint32_t ops = si.g == 1 ? (W_BYTES + C::A_BYTES) / 4 * 3 : (W_BYTES + C::A_BYTES);
-        ptx::mbar_arrive_expect_tx(fb, ops + 2u * si.atoms * 512u);
-        ptx::tma_load_2d(ptx::smem_u32(sW + stage * W_BYTES), tw[si.g], fb, si.kcoord, nt * 128);
-        ptx::tma_load_2d(ptx::smem_u32(sA + stage * C::A_BYTES), ta[si.g], fb, si.kcoord, 0);
-        uint8_t* sf = sSF + stage * 2 * C::SF_BYTES;
-        ptx::bulk_load(ptx::smem_u32(sf), p.sfw[si.g] + ((int64_t)nt * kp128 + si.atom0) * 512, si.atoms * 512, fb);
-        ptx::bulk_load(ptx::smem_u32(sf + C::SF_BYTES), p.sfa[si.g] + (int64_t)si.atom0 * 512, si.atoms * 512, fb);
+        if (ops_w) {
+          ptx::mbar_arrive_expect_tx(fb, ops + 2u * si.atoms * 512u);
+          ptx::tma_load_2d(ptx::smem_u32(sW + stage * W_BYTES), tw[si.g], fb, si.kcoord, nt * 128);
+          ptx::tma_load_2d(ptx::smem_u32(sA + stage * C::A_BYTES), ta[si.g], fb, si.kcoord, 0);
+        } else {
+          uint8_t* sf = sSF + stage * 2 * C::SF_BYTES;
+          ptx::bulk_load(ptx::smem_u32(sf), p.sfw[si.g] + ((int64_t)nt * kp128 + si.atom0) * 512, si.atoms * 512, fb);
+          ptx::bulk_load(ptx::smem_u32(sf + C::SF_BYTES), p.sfa[si.g] + (int64_t)si.atom0 * 512, si.atoms * 512, fb);
+        }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
