@@ -147,8 +147,11 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
 
   const int nstages = p.nst[0] + p.nst[1] + p.nst[2];
 
-  if (warp == 0) {
-    // ============================ TMA producer ============================
+  if (warp == 0 || warp == 3) {
+    // ============================ TMA producers ============================
+    // warp 0: transaction count + A and W tiles; warp 3: the scale atoms (two issuing
+    // threads, as in the CTA-pair kernel).
+    const bool ops = warp == 0;
     if (lane == 0) {
       const CUtensorMap* ta[3] = {&ta0, &ta1, &ta2};
       const CUtensorMap* tb[3] = {&tb0, &tb1, &tb2};
@@ -171,9 +174,13 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
           for (int rg = 0; rg < C::RG; ++rg)
             if ((int64_t)(n0 / 128 + rg) * 128 < p.sfb_rows_pad) ++nrg;
           bytes += nrg * si.atoms * 512;
-          ptx::mbar_arrive_expect_tx(fb, bytes);
-          ptx::tma_load_2d(ptx::smem_u32(sA + stage * C::A_BYTES), ta[si.g], fb, si.kcoord, m0);
-          ptx::tma_load_2d(ptx::smem_u32(sB + stage * C::B_BYTES), tb[si.g], fb, si.kcoord, n0);
+          if (ops) {
+            ptx::mbar_arrive_expect_tx(fb, bytes);
+            ptx::tma_load_2d(ptx::smem_u32(sA + stage * C::A_BYTES), ta[si.g], fb, si.kcoord, m0);
+            ptx::tma_load_2d(ptx::smem_u32(sB + stage * C::B_BYTES), tb[si.g], fb, si.kcoord, n0);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           const uint8_t* a_src = p.sfa[si.g] + ((int64_t)mb * kp128 + si.atom0) * 512;
           ptx::bulk_load(ptx::smem_u32(sSFA + stage * C::SFA_BYTES), a_src, si.atoms * 512, fb);
           for (int rg = 0; rg < nrg; ++rg) {
