@@ -368,11 +368,14 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       const int wrow = 128 * (int)rank + q * 32 + lane;   // row inside the 256-row pair tile
       if (from_ws) {   // wait until the previous pair's 8 epilogue warps published its partial
         if (lane == 0) {
-          volatile int* f = p.ws_flag + (pair - 1);
-          while (*f < 8) __nanosleep(64);
+          int v;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.ws_flag + (pair - 1)) : "memory");
+            if (v >= 8) break;
+            __nanosleep(64);
+          }
         }
-        __syncwarp();
-        __threadfence();
+        __syncwarp();   // the acquire by lane 0 is made cumulative for the warp
       }
       const int acc = it & 1;
       ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), (it >> 1) & 1, 24, it, t);
@@ -459,9 +462,8 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         ++nstore;
       }
       if (to_ws) {   // publish: this warp's rows of the partial are in global memory
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicAdd(p.ws_flag + pair, 1);
+        __syncwarp();   // orders the other lanes' stores before lane 0's release
+        if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.ws_flag + pair) : "memory");
       }
       if (from_ws) {  // consumed: hand the slot back (8 x -1 returns it to 0)
         __syncwarp();
