@@ -156,7 +156,8 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   uint64_t* tfull = bars + 2 * STAGES;    // [2] per accumulator (each CTA)
   uint64_t* tempty = tfull + 2;           // [2] accumulator fully drained (even CTA)
   uint64_t* tovl = tempty + 2;            // [2] overlap columns drained (even CTA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tovl + 2);
+  uint64_t* pbar = tovl + 2;              // [4] stream-K: a warp's partial rows landed in smem
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();    // 0 = MMA leader
@@ -179,6 +180,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       ptx::mbar_init(ptx::smem_u32(&tfull[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&tempty[i]), 8);   // 4 epilogue warps x 2 CTAs
       ptx::mbar_init(ptx::smem_u32(&tovl[i]), 8);
+    }
+    for (int i = 0; i < 4; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&pbar[i]), 1);
     }
     ptx::fence_barrier_init();
   }
@@ -379,6 +383,21 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       }
       const int acc = it & 1;
       ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), (it >> 1) & 1, 24, it, t);
+      // Stream-K tail: this is the pair's last item, so once its MMAs are done the
+      // operand ring is idle.  The warp's 32 partial rows (contiguous 32 KB in the
+      // workspace) are staged there with ONE bulk copy, instead of eight dependent
+      // rounds of global loads (one per 32-column chunk) in the drain loop.
+      const uint8_t* pst = nullptr;
+      if (from_ws) {
+        uint8_t* dstp = sA + q * 32768;   // sA and sB are contiguous: >= 128 KB for >= 4 stages
+        const uint32_t pb = ptx::smem_u32(&pbar[q]);
+        if (lane == 0) {
+          ptx::mbar_arrive_expect_tx(pb, 32768);
+          ptx::bulk_load(ptx::smem_u32(dstp), p.ws + ((size_t)(pair - 1) * 256 + 128 * (int)rank + q * 32) * 256, 32768, pb);
+        }
+        ptx::mbar_wait(pb, 0, 28, it, t);
+        pst = dstp;
+      }
       if (trace && q == 0 && it < 3) g_trace[blockIdx.x][9 + it] = ptx::globaltimer_ns();
       if (trace && q == 0 && it == 0 && rank == 0) g_trace[blockIdx.x][21] = clock64();
       ptx::tc_fence_after();
@@ -427,10 +446,10 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
           continue;
         }
         if (from_ws) {   // add the previous pair's partial (fixed order: partial + own)
-          const float4* src = reinterpret_cast<const float4*>(p.ws + ((size_t)(pair - 1) * 256 + wrow) * 256 + 32 * c);
+          const float4* src = reinterpret_cast<const float4*>(pst + lane * 1024 + 128 * c);
 #pragma unroll
           for (int v = 0; v < 8; ++v) {
-            const float4 o = __ldcg(src + v);
+            const float4 o = src[v];
             r[4 * v] = __float_as_uint(o.x + __uint_as_float(r[4 * v]));
             r[4 * v + 1] = __float_as_uint(o.y + __uint_as_float(r[4 * v + 1]));
             r[4 * v + 2] = __float_as_uint(o.z + __uint_as_float(r[4 * v + 2]));
@@ -602,7 +621,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
       return cudaErrorMemoryAllocation;
     }
   }
-  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + epi_bytes<STAGES>() + (2 * STAGES + 6) * 8 + 16;
+  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + epi_bytes<STAGES>() + (2 * STAGES + 10) * 8 + 16;
   auto kern = mixgemm2_kernel<STAGES, NP>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
