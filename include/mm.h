@@ -260,8 +260,11 @@ mm_status mm_mixed_gemm_bf16_nshard_allgather(const mm_mx_tensor* a, const mm_mx
  * ldy % 8 == 0.  barrier = 1 appends the flag barrier on `stream` (the call then
  * completes on every rank only when all ranks have called it: a collective);
  * barrier = 0 leaves it to mm_peer_barrier (same-process virtual ranks, where the
- * barriers of all ranks must run concurrently on different streams).  Errors as
- * everywhere: validated before any launch, nothing enqueued on error. */
+ * barriers of all ranks must run concurrently on different streams).  Y reuse: peers
+ * write into this rank's Y as soon as they reach the call, so a rank that still reads
+ * its previous Y must separate iterations with mm_peer_barrier (or alternate two
+ * windows).  Errors as everywhere: validated before any launch, nothing enqueued on
+ * error. */
 size_t mm_peer_buffer_bytes(int64_t M, int64_t ldy);
 int32_t mm_ipc_handle_bytes(void);                                   /* 72 */
 mm_status mm_ipc_get_handle(const void* d_buf, void* h_handle_out);   /* 64 B CUDA IPC handle of the
@@ -270,7 +273,8 @@ mm_status mm_peer_window_open(int32_t rank, int32_t world, void* d_local_buf, co
                               int64_t M, int64_t ldy, void** win_out);
 mm_status mm_peer_window_from_ptrs(int32_t rank, int32_t world, void* const* h_dev_bufs, int64_t M,
                                    int64_t ldy, void** win_out);
-mm_status mm_peer_window_close(void* win);
+mm_status mm_peer_window_close(void* win);   /* no queued work may still use the window, on
+                                                any rank (e.g. close after a final barrier) */
 mm_status mm_mixed_gemm_bf16_nshard_peerstore(const mm_mx_tensor* a, const mm_mx_tensor* w_shard,
                                               const mm_plan* plan, int64_t n_total, void* win,
                                               int32_t barrier, mm_stream_t stream);
