@@ -187,3 +187,52 @@ def test_rel_fro_budget_of_bf16_rounding():
     y = rng.standard_normal((256, 1024)) @ rng.standard_normal((256, 1024)).T
     e = gemm.rel_fro(mx.bf16_rne(y), y)
     assert 1.4e-3 < e < 1.9e-3
+
+
+def test_eq6_violations_hand_built_case():
+    """eq6_violations (R13: counts by max (Eq. 6), order by mean
+    (Eq. 7), violations = channels whose max exceeds the threshold of the
+    group the mean ordering put them in) on a case whose answer is fixed by hand."""
+    t4, t6 = 1.0, 4.0
+    # 8 channels; the mean order (perm) puts channels 5, 2, 7 in P4, channels 0, 3 in
+    # P6 and channels 1, 4, 6 in P8.
+    chmax = np.array([5.0, 9.0, 1.0, 3.0, 0.5, 0.25, 7.0, 1.5])
+    perm = np.array([5, 2, 7, 0, 3, 1, 4, 6])
+    n = (3, 2, 3)
+    # P4 = {5: 0.25 ok, 2: 1.0 ok (<= T4 is allowed), 7: 1.5 > 1 -> violation}
+    # P6 = {0: 5.0 > 4 -> violation, 3: 3.0 ok}; P8 is never a violation
+    assert calib.eq6_violations(perm, n, chmax, t4, t6) == (1, 1)
+    # all channels placed in their own Eq. 6 group -> none
+    perm2 = np.array([5, 4, 2, 3, 7, 0, 1, 6])
+    assert calib.eq6_violations(perm2, n, chmax, t4, t6) == (0, 0)   # P4 {0.25,.5,1}; P6 {3,1.5}
+    # everything in P4: every channel with max > T4 violates
+    assert calib.eq6_violations(np.arange(8), (8, 0, 0), chmax, t4, t6) == (int(np.sum(chmax > t4)), 0)
+
+
+def test_eq6_violations_brute_force_recount():
+    """Recount position by position (which group does reordered position j fall in,
+    does its channel's max exceed that group's threshold) on random plans."""
+    rng = np.random.default_rng(7)
+    for trial in range(20):
+        K = 32 * int(rng.integers(1, 9))
+        chmax = mx.bf16_rne(np.abs(rng.standard_normal(K)) * 3)
+        t4, t6 = 0.8, 2.5
+        perm = rng.permutation(K)
+        a = 32 * int(rng.integers(0, K // 32 + 1))
+        b = 32 * int(rng.integers(0, (K - a) // 32 + 1))
+        n = (a, b, K - a - b)
+        v4 = v6 = 0
+        for j in range(K):
+            m = chmax[perm[j]]
+            if j < n[0]:
+                v4 += int(m > t4)
+            elif j < n[0] + n[1]:
+                v6 += int(m > t6)
+        assert calib.eq6_violations(perm, n, chmax, t4, t6) == (v4, v6), trial
+    # a calibrated plan: mean order vs max thresholds disagree somewhere on the
+    # synthetic profile, and the count is consistent with Eq. 6 (violations in P4
+    # can only come from channels Eq. 6 put in P6/P8)
+    x = bf16_bits(gen_act(1024, 1024, 1000, 2000))
+    c = calib.calibrate(x)
+    v4, v6 = calib.eq6_violations(c["perm"], c["n"], c["chmax"], c["t4"], c["t6"])
+    assert v4 <= c["c"][1] + c["c"][2] and v6 <= c["c"][2] + c["n"][1]

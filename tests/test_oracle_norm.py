@@ -55,3 +55,43 @@ def test_against_torch_fp64_rms():
     # and the unrounded oracle agrees with torch to fp64 accuracy
     yf = onorm.rmsnorm_f64(bf16_bits(x), bf16_bits(g), eps)
     assert np.allclose(yf, ref.numpy(), rtol=1e-12, atol=0)
+
+
+def _hf_llama_rmsnorm(x_bf16, gamma_bf16, r_f32):
+    """The literal HF LlamaRMSNorm forward in torch (CPU), with the row scale r
+    injected instead of torch.rsqrt(variance + eps) (whose fp32 rounding is not
+    what R27 fixes):  hidden = x.to(float32); hidden = hidden * r;
+    return weight * hidden.to(bfloat16)."""
+    hidden = x_bf16.to(torch.float32)
+    hidden = hidden * r_f32[:, None]
+    return gamma_bf16 * hidden.to(torch.bfloat16)
+
+
+def test_rounding_order_matches_literal_hf_expression():
+    """Reading R27's order of roundings -- t = bf16(fp32(x * r)) BEFORE the gamma
+    multiply, then bf16(gamma * t) -- equals the literal HF expression bit for bit,
+    and is distinguishable from the one-rounding alternative bf16(x * r * gamma)."""
+    eps = 1e-5
+    for K, seed in ((1024, 1), (4096, 2), (320, 3)):
+        x = gen_act(16, K, 1000 + seed, 2100 + seed)
+        g = gen_uniform_bf16((K,), 0.25, 2.0, 40 + seed)
+        xb, gb = bf16_bits(x), bf16_bits(g)
+        r = torch.tensor([float(onorm.row_scale_f32(xb[i], K, eps)) for i in range(x.shape[0])],
+                         dtype=torch.float32)
+        want = bf16_bits(_hf_llama_rmsnorm(x, g, r))
+        got = onorm.rmsnorm_bf16_bits(xb, gb, eps)
+        assert np.array_equal(got, want), K
+        # the single-rounding alternative differs on these inputs (the pin discriminates)
+        alt = bf16_bits((x.to(torch.float64) * r.double()[:, None] * g.double()).to(torch.bfloat16))
+        assert not np.array_equal(alt, want), K
+
+
+def test_row_scale_matches_torch_fp64():
+    """r = fp32(1/sqrt(ss/K + eps)) against torch's fp64 sum of squares (a library
+    reduction; equal after the fp32 rounding except on astronomically rare ties)."""
+    for K, seed in ((256, 5), (4096, 6), (14336, 7)):
+        x = gen_act(8, K, 1000 + seed, 2200 + seed)
+        xd = x.double()
+        rt = (1.0 / torch.sqrt(xd.pow(2).sum(-1) / K + 1e-6)).float()
+        ro = [onorm.row_scale_f32(bf16_bits(x)[i], K, 1e-6) for i in range(8)]
+        assert np.array_equal(np.array(ro, dtype=np.float32), rt.numpy()), K
