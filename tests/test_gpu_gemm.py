@@ -70,7 +70,11 @@ def _int_operand(rows, n, rng, kind):
 
 @pytest.mark.parametrize("M,N,n,bn", [(128, 256, (256, 128, 128), 0), (200, 272, (96, 160, 224), 0),
                                       (64, 512, (1024, 512, 256), 0), (24, 512, (1024, 512, 256), 0),
-                                      (128, 384, (256, 128, 128), 1)])
+                                      (128, 384, (256, 128, 128), 1),
+                                      # the production CTA-pair kernel (mixgemm2_kernel): auto at M > 128,
+                                      # forced at M = 128; several pair tiles, ragged M and N tails
+                                      (256, 512, (256, 128, 128), 0), (128, 256, (256, 128, 128), 512),
+                                      (600, 784, (2240, 1184, 672), 0), (2048, 1024, (512, 256, 256), 512)])
 def test_exact_integer_case_bit_exact(M, N, n, bn):
     """P-I(i): all products and partial sums are integers < 2^24, so FP32
     accumulation is exact in any order and Y must equal bf16(Y_exact) bit for bit."""
@@ -99,8 +103,9 @@ def test_exact_integer_case_bit_exact(M, N, n, bn):
     assert len(bad) == 0, (len(bad), bad[:5], y.cpu().double().numpy()[tuple(bad[0])], exact[tuple(bad[0])])
 
 
+@pytest.mark.parametrize("M,bn", [(128, 0), (256, 0), (128, 512), (256, 512)])
 @pytest.mark.parametrize("seg", [0, 1, 2])
-def test_one_hot_layout_probe(seg):
+def test_one_hot_layout_probe(seg, M, bn):
     """P-L: row m of A is one-hot at reordered column j(m) (value 1.0, exact in
     every format); W has distinct small integers per column, so Y[m, :] reveals
     which column the tensor core decoded -- pins FP4 nibble order, FP6 bit order
@@ -108,7 +113,7 @@ def test_one_hot_layout_probe(seg):
     n = [0, 0, 0]
     n[seg] = 256
     K = 256
-    M, N = 128, 256
+    N = 256
     perm = np.arange(K)
     rng = np.random.default_rng(seg)
     jsel = rng.permutation(K)[:M]
@@ -119,7 +124,11 @@ def test_one_hot_layout_probe(seg):
     top = (6.0, 28.0, 256.0)[seg]
     wa[:, ::32] = top
     plan = mm.mm_plan_init(K, tuple(n), perm)
-    y = _run(bits_to_bf16(omx.bf16_rne_bits(xa)), bits_to_bf16(omx.bf16_rne_bits(wa)), plan)
+    mm.mm_set_gemm_config(bn, 0, 0)    # M = 128: auto = small-M kernel; bn = 512 / M = 256: the CTA-pair kernel
+    try:
+        y = _run(bits_to_bf16(omx.bf16_rne_bits(xa)), bits_to_bf16(omx.bf16_rne_bits(wa)), plan)
+    finally:
+        mm.mm_set_gemm_config(0, 0, 0)
     yc = y.double().cpu().numpy()
     # every product is exact (one-hot 1.0 x small integers, e = 0): Y[m, :] must be
     # exactly column jsel[m] of W (columns that happen to be equal are equivalent)
@@ -152,9 +161,11 @@ def test_variants(fmt6, fmt8, rule):
     _check(y, yref, ybf)
 
 
-@pytest.mark.parametrize("bn,stages", [(128, 6), (256, 4)])
+@pytest.mark.parametrize("bn,stages", [(0, 0), (512, 0), (128, 6), (256, 4)])
 def test_qproj_full_size(bn, stages):
-    """Config 2, Llama-3.1-8B q_proj, calibrated plan, full fp64 oracle."""
+    """Config 2, Llama-3.1-8B q_proj, calibrated plan, full fp64 oracle: the
+    automatic dispatch (= the CTA-pair kernel the bench times), the pair kernel
+    forced, and the single-CTA 128/256-wide tiles."""
     mm.mm_set_gemm_config(bn, stages, 0)
     try:
         plan = mm.mm_calibrate_thresholds(gen_act(4096, 4096, 1000, 2000).cuda())

@@ -4,11 +4,15 @@ a world-size-1 communicator exercises the library's NCCL binding, the staging
 layout and the [G][M][N/G] -> [M][N] permute; the result must equal the unsharded
 mm_mixed_gemm_bf16 output bit for bit (same tiles, same K order).  The world-size-2
 host logic is covered on CPU by tests/test_dist_gloo.py."""
+import numpy as np
 import pytest
 import torch
 
 import paper_2508_02343_b200 as mm
-from synth import gen_act, gen_perm, gen_weight
+from oracle import gemm as ogemm
+from synth import bf16_bits, gen_act, gen_perm, gen_weight
+
+from accuracy import ref_and_abs, report
 
 pytestmark = pytest.mark.gpu
 
@@ -17,8 +21,9 @@ pytestmark = pytest.mark.gpu
 def test_nshard_world1_equals_plain(M, N, n):
     K = sum(n)
     plan = mm.mm_plan_init(K, n, gen_perm(K, 21))
-    a = mm.mm_reorder_quantize_act(gen_act(M, K, 1000, 2001).cuda(), plan)
-    w = mm.mm_quantize_weight_offline(gen_weight(N, K, 3000).cuda(), plan)
+    x, wb = gen_act(M, K, 1000, 2001), gen_weight(N, K, 3000)
+    a = mm.mm_reorder_quantize_act(x.cuda(), plan)
+    w = mm.mm_quantize_weight_offline(wb.cuda(), plan)
     y_plain = mm.mm_mixed_gemm_bf16(a, w, plan)
     comm = mm.mm_comm_init(0, 1, mm.nccl_unique_id())
     try:
@@ -27,6 +32,19 @@ def test_nshard_world1_equals_plain(M, N, n):
     finally:
         mm.mm_comm_destroy(comm)
     assert torch.equal(y_plain.view(torch.int16), y_shard.view(torch.int16))
+    # and against the oracle (sampled rows x all columns, every element inside the
+    # worst-case FP32 bound of tests/accuracy.py, relative Frobenius <= 2e-3)
+    rows = np.arange(0, M, 3)
+    yref, S = ref_and_abs(bf16_bits(x)[rows], bf16_bits(wb), plan.perm_host().numpy(), plan.n,
+                          *_fmts(plan))
+    r = report(bf16_bits(y_shard.cpu())[rows], yref, S, K)
+    assert r["bound_violations"] == 0 and r["rel_fro"] <= 2e-3, r
+
+
+def _fmts(plan):
+    from oracle.formats import E2M3, E3M2, E4M3, E5M2
+    return ({mm.MM_E3M2: E3M2, mm.MM_E2M3: E2M3}[plan.fmt6], {mm.MM_E4M3: E4M3, mm.MM_E5M2: E5M2}[plan.fmt8],
+            plan.rule)
 
 
 def test_nshard_rejects_bad_shapes():

@@ -10,25 +10,41 @@ for bit (same tiles, same K order), columns beyond n_total untouched.  The CUDA
 IPC path (mm_ipc_get_handle / mm_peer_window_open) is exercised at world size 1
 and for the handle's sub-allocation offset; the world-2 handle exchange runs on
 CPU in tests/test_dist_gloo.py."""
+import numpy as np
 import pytest
 import torch
 
 import paper_2508_02343_b200 as mm
-from synth import gen_act, gen_perm, gen_weight
+from synth import bf16_bits, gen_act, gen_perm, gen_weight
+
+from accuracy import ref_and_abs, report
 
 pytestmark = pytest.mark.gpu
 
 
-def _setup(M, Ns, G, n, seed=31):
+def _setup(M, Ns, G, n, seed=31, with_inputs=False):
     K = sum(n)
     N = Ns * G
     plan = mm.mm_plan_init(K, n, gen_perm(K, seed))
-    a = mm.mm_reorder_quantize_act(gen_act(M, K, 1000, 2001).cuda(), plan)
+    x = gen_act(M, K, 1000, 2001)
+    a = mm.mm_reorder_quantize_act(x.cuda(), plan)
     w = gen_weight(N, K, 3000).cuda()
     w_full = mm.mm_quantize_weight_offline(w, plan)
     shards = [mm.mm_quantize_weight_offline(w[r * Ns:(r + 1) * Ns].contiguous(), plan) for r in range(G)]
     y_ref = mm.mm_mixed_gemm_bf16(a, w_full, plan)
+    if with_inputs:
+        return plan, a, shards, y_ref, x, w.cpu()
     return plan, a, shards, y_ref
+
+
+def _oracle_check(y, x, w, plan, rows):
+    """Sampled rows of a gathered Y against the fp64 oracle (tests/accuracy.py bars)."""
+    from oracle.formats import E2M3, E3M2, E4M3, E5M2
+    f6 = {mm.MM_E3M2: E3M2, mm.MM_E2M3: E2M3}[plan.fmt6]
+    f8 = {mm.MM_E4M3: E4M3, mm.MM_E5M2: E5M2}[plan.fmt8]
+    yref, S = ref_and_abs(bf16_bits(x)[rows], bf16_bits(w), plan.perm_host().numpy(), plan.n, f6, f8, plan.rule)
+    r = report(bf16_bits(y.cpu())[rows], yref, S, sum(plan.n))
+    assert r["bound_violations"] == 0 and r["rel_fro"] <= 2e-3, r
 
 
 def _virtual_ranks(plan, a, shards, M, Ns, G, ldy, iters=2):
@@ -56,13 +72,15 @@ def _virtual_ranks(plan, a, shards, M, Ns, G, ldy, iters=2):
                                       (520, 512, 8, (512, 256, 256)), (64, 96, 2, (128, 64, 64)),
                                       (2048, 512, 8, (2240, 1184, 672)), (130, 272, 3, (0, 256, 0))])
 def test_peerstore_virtual_ranks_equal_1gpu(M, Ns, G, n):
-    plan, a, shards, y_ref = _setup(M, Ns, G, n)
+    plan, a, shards, y_ref, x, w = _setup(M, Ns, G, n, with_inputs=True)
     N = Ns * G
     ldy = N + 8                        # a column beyond n_total must stay untouched
     ys, _ = _virtual_ranks(plan, a, shards, M, Ns, G, ldy)
     for r, y in enumerate(ys):
         assert torch.equal(y[:, :N].view(torch.int16), y_ref.view(torch.int16)), f"rank {r} Y differs"
         assert not y[:, N:].view(torch.int16).any(), f"rank {r}: columns past n_total written"
+    # the gathered output against the oracle (every 5th row, all N columns)
+    _oracle_check(ys[-1][:, :N].contiguous(), x, w, plan, np.arange(0, M, 5))
 
 
 def test_peerstore_world1_ipc_window():
