@@ -24,7 +24,9 @@
  *    has been enqueued and mm_last_error() (thread-local) has the reason.
  *  - Pointers named d_* are DEVICE pointers, h_* are HOST pointers.  All
  *    buffers are allocated and owned by the caller; the library allocates no
- *    device memory on the hot calls and keeps no reference after the work
+ *    device memory and never synchronizes on the hot calls (mm_reorder_quantize_act,
+ *    mm_rmsnorm_reorder_quantize_act, mm_mixed_gemm_bf16 and the N-shard GEMMs), so
+ *    they can be captured into CUDA graphs; it keeps no reference after the work
  *    queued on `stream` has completed (buffers are borrowed until then).
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
  *    asynchronous on that stream except where stated.
@@ -193,15 +195,23 @@ mm_status mm_rmsnorm_reorder_quantize_act(const void* d_x, int64_t M, int64_t ld
  * K-segments, one FP32 accumulator, BF16 round-to-nearest-even output
  * (row-major, ld = ldy >= N, ldy % 8 == 0).  A and W must come from `plan`
  * (fingerprints equal) -- else MM_ERR_PLAN_MISMATCH.  N % 16 == 0.
- * Small M (<= 32, or <= 128 with a long K loop) runs the swap-AB / split-K kernel:
- * each K split keeps its own FP32 accumulator and the partials are added in split
- * order (deterministic; reading R28).  Its FP32 partials live in a
- * library-owned workspace per (device, stream), allocated on the first such call
- * and grown on demand (<= num_tiles x 4 splits x 64 KB; this is the one allocation a
- * hot call can make, once). */
+ * Small M (<= 128 when the W tiles leave room for >= 2 K splits) runs the swap-AB /
+ * split-K kernel: each K split keeps its own FP32 accumulator and the partials are
+ * added in split order (deterministic; reading R28).  Its FP32 partials
+ * and arrival counters (and those of the opt-in stream-K schedule) live in the
+ * CALLER's workspace d_ws of ws_bytes >= mm_gemm_workspace_bytes(plan, M, N) bytes:
+ * 256-byte aligned, ZERO-FILLED once before its first use (the kernels leave every
+ * counter at zero), reusable by later calls on the same stream, not shared by calls
+ * in flight on different streams.  d_ws may be NULL when the query returns 0.
+ * Errors: MM_ERR_WORKSPACE if the workspace is missing, misaligned or too small. */
 mm_status mm_mixed_gemm_bf16(const mm_mx_tensor* a, const mm_mx_tensor* w,
                              const mm_plan* plan, void* d_y, int64_t ldy,
-                             mm_stream_t stream);
+                             void* d_ws, size_t ws_bytes, mm_stream_t stream);
+
+/* Workspace bytes mm_mixed_gemm_bf16 needs for an M x N output under the current
+ * tile configuration (mm_set_gemm_config); 0 when the chosen kernel needs none;
+ * -1 on an invalid plan or negative sizes.  Pure host function. */
+int64_t mm_gemm_workspace_bytes(const mm_plan* plan, int64_t M, int64_t N);
 
 /* Test entry: the reorder output x_r[m, j] = X[m, perm[j]] as BF16 [M, K]
  * (ld = ldxr), for bit-exact reorder parity.  Not on the hot path. */
@@ -229,13 +239,16 @@ int32_t mm_nccl_unique_id_bytes(void);                       /* 128 */
 mm_status mm_nccl_get_unique_id(void* h_id_out);            /* rank 0 only */
 mm_status mm_comm_init(int32_t rank, int32_t world, const void* h_unique_id, void** comm_out);
 mm_status mm_comm_destroy(void* comm);
-/* d_stage: caller scratch of >= 2*M*N bytes (BF16 [G][M][N/G]).  Y shard is
- * computed into the stage slot of this rank, all-gathered, then permuted into
- * d_y_full [M, N] (ld = ldy). */
+/* d_stage: caller scratch of stage_bytes >= 2*M*N bytes (BF16 [G][M][N/G]),
+ * 16-byte aligned.  Y shard is computed into the stage slot of this rank,
+ * all-gathered, then permuted into d_y_full [M, N] (ld = ldy, 16-byte aligned).
+ * The shard GEMM uses no workspace (tile kernels only).  Errors
+ * (MM_ERR_SHAPE / _ALIGNMENT / _WORKSPACE / _NCCL) are detected before anything is
+ * enqueued. */
 mm_status mm_mixed_gemm_bf16_nshard_allgather(const mm_mx_tensor* a, const mm_mx_tensor* w_shard,
                                               const mm_plan* plan, int64_t n_total,
                                               void* d_y_full, int64_t ldy, void* d_stage,
-                                              void* comm, mm_stream_t stream);
+                                              size_t stage_bytes, void* comm, mm_stream_t stream);
 
 /* ---- fused GEMM + all-gather epilogue over peer memory ----
  * The N-shard of mm_mixed_gemm_bf16_nshard_allgather without a separate
@@ -246,7 +259,7 @@ mm_status mm_mixed_gemm_bf16_nshard_allgather(const mm_mx_tensor* a, const mm_mx
  *
  * Peer buffer (one per rank, caller-allocated, 256-B aligned, ZERO-FILLED before
  * the handle exchange, e.g. torch.zeros): [Y: BF16 M x ldy, padded to 256 B]
- * [flags: 64 x u32].  mm_peer_buffer_bytes gives its size.
+ * [flags: 64 x u32; word 63 = barrier-timeout record].  mm_peer_buffer_bytes gives its size.
  *
  * Window: this rank's table of all ranks' buffers.  mm_peer_window_open maps the
  * peers' buffers from CUDA IPC handles (mm_ipc_get_handle on each rank, exchanged
@@ -279,6 +292,13 @@ mm_status mm_mixed_gemm_bf16_nshard_peerstore(const mm_mx_tensor* a, const mm_mx
                                               const mm_plan* plan, int64_t n_total, void* win,
                                               int32_t barrier, mm_stream_t stream);
 mm_status mm_peer_barrier(void* win, mm_stream_t stream);
+/* Barrier timeout of a window (default 0 = wait forever, like NCCL: a slow rank is
+ * not an error).  With a timeout, a barrier whose peer never arrives gives up, and
+ * records the missing rank in this rank's buffer instead of trapping (the CUDA
+ * context stays usable); mm_peer_window_error (synchronous read, call after the
+ * stream completed) returns it in *h_missing_rank, or -1 if every barrier completed. */
+mm_status mm_peer_window_set_timeout(void* win, double seconds);
+mm_status mm_peer_window_error(void* win, int32_t* h_missing_rank);
 
 #ifdef __cplusplus
 }

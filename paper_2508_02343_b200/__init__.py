@@ -32,7 +32,8 @@ SEG_BITS = (4, 6, 8)
 EXPORTS = [
     "mm_padded_cols", "mm_code_pitch_bytes", "mm_codes_bytes", "mm_sf_bytes",
     "mm_calib_workspace_bytes", "mm_plan_init", "mm_calibrate_thresholds",
-    "mm_quantize_weight_offline", "mm_reorder_quantize_act", "mm_mixed_gemm_bf16",
+    "mm_quantize_weight_offline", "mm_reorder_quantize_act", "mm_mixed_gemm_bf16", "mm_gemm_workspace_bytes",
+    "mm_peer_window_set_timeout", "mm_peer_window_error",
     "mm_reorder_act_bf16", "mm_set_gemm_config", "mm_launch_count", "mm_reset_launch_count",
     "mm_last_error", "mm_abi_version", "mm_nccl_unique_id_bytes", "mm_nccl_get_unique_id",
     "mm_comm_init", "mm_comm_destroy", "mm_mixed_gemm_bf16_nshard_allgather",
@@ -96,7 +97,8 @@ def lib(build_if_missing: bool = False):
                                                        ctypes.c_size_t, vp, vp, vp]),
             "mm_quantize_weight_offline": (ctypes.c_int, [vp, i64, i64, P, X, vp]),
             "mm_reorder_quantize_act": (ctypes.c_int, [vp, i64, i64, P, X, vp]),
-            "mm_mixed_gemm_bf16": (ctypes.c_int, [X, X, P, vp, i64, vp]),
+            "mm_mixed_gemm_bf16": (ctypes.c_int, [X, X, P, vp, i64, vp, ctypes.c_size_t, vp]),
+            "mm_gemm_workspace_bytes": (i64, [P, i64, i64]),
             "mm_reorder_act_bf16": (ctypes.c_int, [vp, i64, i64, P, vp, i64, vp]),
             "mm_set_gemm_config": (ctypes.c_int, [i32, i32, i32]),
             "mm_launch_count": (i64, []),
@@ -107,7 +109,8 @@ def lib(build_if_missing: bool = False):
             "mm_nccl_get_unique_id": (ctypes.c_int, [vp]),
             "mm_comm_init": (ctypes.c_int, [i32, i32, vp, ctypes.POINTER(vp)]),
             "mm_comm_destroy": (ctypes.c_int, [vp]),
-            "mm_mixed_gemm_bf16_nshard_allgather": (ctypes.c_int, [X, X, P, i64, vp, i64, vp, vp, vp]),
+            "mm_mixed_gemm_bf16_nshard_allgather": (ctypes.c_int, [X, X, P, i64, vp, i64, vp, ctypes.c_size_t,
+                                                                   vp, vp]),
             "mm_calib_state_bytes": (i64, [i32]),
             "mm_calib_accumulate": (ctypes.c_int, [vp, i64, i32, i64, vp, ctypes.c_size_t, vp, vp]),
             "mm_calib_finalize": (ctypes.c_int, [vp, i32, i32, i32, i32, vp, P, vp, vp, vp, vp]),
@@ -121,6 +124,8 @@ def lib(build_if_missing: bool = False):
             "mm_peer_window_close": (ctypes.c_int, [vp]),
             "mm_mixed_gemm_bf16_nshard_peerstore": (ctypes.c_int, [X, X, P, i64, vp, i32, vp]),
             "mm_peer_barrier": (ctypes.c_int, [vp, vp]),
+            "mm_peer_window_set_timeout": (ctypes.c_int, [vp, ctypes.c_double]),
+            "mm_peer_window_error": (ctypes.c_int, [vp, ctypes.POINTER(i32)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -311,13 +316,45 @@ def mm_rmsnorm_reorder_quantize_act(x: torch.Tensor, gamma: torch.Tensor, eps: f
     return out
 
 
+def mm_gemm_workspace_bytes(plan: Plan, M: int, N: int) -> int:
+    n = int(lib().mm_gemm_workspace_bytes(ctypes.byref(plan.c), M, N))
+    if n < 0:
+        raise MMError(1, "mm_gemm_workspace_bytes: invalid arguments")
+    return n
+
+
+_WS = {}   # (device index, stream handle) -> zero-filled uint8 workspace (grown, never shrunk)
+
+
+def gemm_workspace(plan: Plan, M: int, N: int, stream=None) -> torch.Tensor | None:
+    """The caller-owned GEMM workspace (include/mm.h) this binding keeps per (device,
+    stream): allocated by torch, zero-filled once, grown when a larger one is needed.
+    Call it once before capturing a CUDA graph so the capture allocates nothing."""
+    need = mm_gemm_workspace_bytes(plan, M, N)
+    if need == 0:
+        return None
+    dev = plan.d_perm.device
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    key = (dev.index, int(s.cuda_stream))
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < need:
+        if ws is not None:
+            s.synchronize()    # the old buffer may still be in use by queued work
+        ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+        torch.cuda.current_stream(dev).synchronize()
+        _WS[key] = ws
+    return ws
+
+
 def mm_mixed_gemm_bf16(a: MXTensor, w: MXTensor, plan: Plan, out: torch.Tensor | None = None,
-                       stream=None) -> torch.Tensor:
+                       stream=None, workspace: torch.Tensor | None = None) -> torch.Tensor:
     if out is None:
         out = torch.empty(a.rows, w.rows, dtype=torch.bfloat16, device=plan.d_perm.device)
     assert out.dtype == torch.bfloat16 and out.stride(1) == 1
+    ws = workspace if workspace is not None else gemm_workspace(plan, a.rows, w.rows, stream)
     _check(lib().mm_mixed_gemm_bf16(ctypes.byref(a.c), ctypes.byref(w.c), ctypes.byref(plan.c), _ptr(out),
-                                    out.stride(0), _stream(stream)))
+                                    out.stride(0), None if ws is None else _ptr(ws),
+                                    0 if ws is None else ws.numel(), _stream(stream)))
     return out
 
 
@@ -368,7 +405,8 @@ def mm_mixed_gemm_bf16_nshard_allgather(a: MXTensor, w_shard: MXTensor, plan: Pl
         stage = torch.empty(a.rows * n_total, dtype=torch.bfloat16, device=dev)
     _check(lib().mm_mixed_gemm_bf16_nshard_allgather(ctypes.byref(a.c), ctypes.byref(w_shard.c),
                                                      ctypes.byref(plan.c), n_total, _ptr(out), out.stride(0),
-                                                     _ptr(stage), comm, _stream()))
+                                                     _ptr(stage), stage.numel() * stage.element_size(), comm,
+                                                     _stream()))
     return out
 
 
@@ -428,6 +466,16 @@ class PeerWindow:
         if self.h is not None:
             _check(lib().mm_peer_window_close(self.h))
             self.h = None
+
+    def set_timeout(self, seconds: float):
+        """Barrier timeout (0 = wait forever, the default)."""
+        _check(lib().mm_peer_window_set_timeout(self.h, float(seconds)))
+
+    def error(self) -> int:
+        """Rank a timed-out barrier waited for, or -1 (synchronous read)."""
+        v = ctypes.c_int32()
+        _check(lib().mm_peer_window_error(self.h, ctypes.byref(v)))
+        return v.value
 
 
 def mm_mixed_gemm_bf16_nshard_peerstore(a: MXTensor, w_shard: MXTensor, plan: Plan, n_total: int,

@@ -30,12 +30,12 @@ __global__ void gather_layout_kernel(const uint4* __restrict__ stage, int G, int
 // Flag barrier of a peer window (NEXT F1): thread j signals "rank `rank` is done" in
 // rank j's flag array (system-scope release, after a system fence so the preceding
 // GEMM's peer stores are performed first), then waits until rank j's flag in this
-// rank's array reaches `epoch` (system-scope acquire).  A peer that never arrives
-// traps after MM_PEER_TIMEOUT_NS instead of hanging the GPU.
-#ifndef MM_PEER_TIMEOUT_NS
-#define MM_PEER_TIMEOUT_NS 20000000000ull
-#endif
-__global__ void peer_barrier_kernel(PeerFlags fl, int rank, int world, uint32_t epoch) {
+// rank's array reaches `epoch` (system-scope acquire).  timeout_ns == 0 waits forever
+// (NCCL's behaviour: a legitimately slow rank must not kill the job); otherwise a
+// peer that never arrives makes the waiting thread record (missing rank + 1) in this
+// rank's error word (flag slot kPeerErrSlot, read by mm_peer_window_error) and return
+// -- no trap, so the context stays usable.
+__global__ void peer_barrier_kernel(PeerFlags fl, int rank, int world, uint32_t epoch, uint64_t timeout_ns) {
   const int j = threadIdx.x;
   if (j >= world) return;
   __threadfence_system();
@@ -46,11 +46,13 @@ __global__ void peer_barrier_kernel(PeerFlags fl, int rank, int world, uint32_t 
     uint32_t v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fl.f[rank] + j) : "memory");
     if ((int32_t)(v - epoch) >= 0) break;
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > MM_PEER_TIMEOUT_NS) {
-      printf("[mm peer barrier] rank %d: rank %d never arrived (epoch %u)\n", rank, j, epoch);
-      __trap();
+    if (timeout_ns) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicCAS(fl.f[rank] + kPeerErrSlot, 0u, (uint32_t)(j + 1));
+        return;
+      }
     }
     __nanosleep(100);
   }
@@ -58,9 +60,9 @@ __global__ void peer_barrier_kernel(PeerFlags fl, int rank, int world, uint32_t 
 
 }  // namespace
 
-cudaError_t launch_peer_barrier(const PeerFlags& fl, int rank, int world, uint32_t epoch, cudaStream_t s,
-                                int64_t* launches) {
-  peer_barrier_kernel<<<1, 32, 0, s>>>(fl, rank, world, epoch);
+cudaError_t launch_peer_barrier(const PeerFlags& fl, int rank, int world, uint32_t epoch, uint64_t timeout_ns,
+                                cudaStream_t s, int64_t* launches) {
+  peer_barrier_kernel<<<1, 32, 0, s>>>(fl, rank, world, epoch, timeout_ns);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -402,31 +402,51 @@ EncodeTiledFn tensor_map_encoder() {
   return fn;
 }
 
-cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
-                              const char** err) {
+// Kernel choice of the dispatcher (shared by the launch and the workspace query).
+enum GemmPath { PATH_SMALLM, PATH_PAIR, PATH_TILE128, PATH_TILE256 };
+static GemmPath choose_path(const GemmArgs& a, const GemmConfig& cfg) {
   int bn = cfg.block_n;
   // auto: CTA-pair 256 x 256 tiles once M fills a pair tile's rows, else single-CTA 128 x 256
   if (bn == 0) bn = a.M > 128 ? 512 : 256;
-  if (a.n_dst > 0) bn = 512;   // the fused all-gather epilogue lives in the CTA-pair kernel
+  if (a.n_dst > 0) return PATH_PAIR;   // the fused all-gather epilogue lives in the CTA-pair kernel
   // small M (decode-like): swap-AB + split-K kernel (gemm_sm.cu), unless a tile
-  // configuration is forced or MM_GEMM_SMALLM=0
+  // configuration is forced, MM_GEMM_SMALLM=0, or the caller's path must not use a
+  // workspace (N-shard entry points).
   // Auto (measured, q_proj N = 4096: M = 1 / 32 / 64 / 128 -> 10 / 13 / 18 / 26 us vs
   // 25-27 us with 128 x 256 tiles): every M <= 128 when few enough 128-row W tiles
   // exist for each to get >= 2 K splits; otherwise the tile kernel.
   // MM_GEMM_SMALLM=1 forces it for any M <= 128, =0 disables it.
   static const int smallm_env = [] { const char* e = getenv("MM_GEMM_SMALLM"); return e ? atoi(e) : -1; }();
   const bool smallm_auto = a.M <= 128 && 2 * ((a.N + 127) / 128) <= sm_count();
-  if (a.n_dst == 0 && a.M <= 128 &&
+  if (!cfg.no_workspace && a.M <= 128 &&
       (cfg.block_n == 1 || (cfg.block_n == 0 && smallm_env != 0 && (smallm_env == 1 || smallm_auto))))
-    return launch_mixed_gemm_smallm(a, cfg, s, launches, err);
+    return PATH_SMALLM;
   if (bn == 1) bn = a.M > 128 ? 512 : 256;   // small-M kernel requested but M > 128
-  if (bn == 512) return launch_mixed_gemm_2cta(a, cfg, s, launches, err);
-  if (bn == 128) {
-    if (cfg.num_stages == 4) return run<128, 4>(a, cfg, s, launches, err);
-    return run<128, 6>(a, cfg, s, launches, err);
+  if (bn == 512) return PATH_PAIR;
+  return bn == 128 ? PATH_TILE128 : PATH_TILE256;
+}
+
+size_t gemm_workspace_bytes(const GemmArgs& a, const GemmConfig& cfg) {
+  if (a.M <= 0 || a.N <= 0) return 0;
+  switch (choose_path(a, cfg)) {
+    case PATH_SMALLM: return smallm_workspace_bytes(a, cfg);
+    case PATH_PAIR: return pair_workspace_bytes(a, cfg);
+    default: return 0;
   }
-  if (cfg.num_stages == 3) return run<256, 3>(a, cfg, s, launches, err);
-  return run<256, 4>(a, cfg, s, launches, err);
+}
+
+cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
+                              const char** err) {
+  switch (choose_path(a, cfg)) {
+    case PATH_SMALLM: return launch_mixed_gemm_smallm(a, cfg, s, launches, err);
+    case PATH_PAIR: return launch_mixed_gemm_2cta(a, cfg, s, launches, err);
+    case PATH_TILE128:
+      if (cfg.num_stages == 4) return run<128, 4>(a, cfg, s, launches, err);
+      return run<128, 6>(a, cfg, s, launches, err);
+    default:
+      if (cfg.num_stages == 3) return run<256, 3>(a, cfg, s, launches, err);
+      return run<256, 4>(a, cfg, s, launches, err);
+  }
 }
 
 }  // namespace mmx

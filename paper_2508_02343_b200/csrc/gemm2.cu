@@ -75,7 +75,8 @@ struct Gemm2Dev {
   int64_t ldy;
   int stream_k;                   // 1: stream-K split of the K loop over pairs (see work_item)
   float* ws;                      // stream-K partial tiles: [npairs][256 rows][256 cols] fp32
-  int* ws_flag;                   // per pair: 8 epilogue warps arrive (+1), the finisher consumes (-1)
+  int* ws_flag;                   // [npairs][8 epilogue warps]: 1 = that warp's 32 partial rows are
+                                  // published; the one reader warp resets it to 0 after consuming
   int ndst;  // output maps used (1, or the peer window's world size)
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
 };
@@ -370,16 +371,27 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       // stream-K roles of this item: leave a partial (head of a tile) / add one (tail)
       const bool to_ws = s1 < S, from_ws = s0 > 0;
       const int wrow = 128 * (int)rank + q * 32 + lane;   // row inside the 256-row pair tile
-      if (from_ws) {   // wait until the previous pair's 8 epilogue warps published its partial
+      // Stream-K hand-off, one flag per writer warp: warp (rank, q) of pair `pair - 1`
+      // wrote exactly the 32 partial rows warp (rank, q) of this pair reads, so each
+      // reader waits on its own writer only and resets that flag after consuming it
+      // (one writer, one reader per flag per launch; the next launch is stream-ordered).
+      int* const my_flag = p.ws_flag + (pair - 1) * 8 + (int)rank * 4 + q;
+      if (from_ws) {
         if (lane == 0) {
-          int v;
-          for (;;) {
-            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.ws_flag + (pair - 1)) : "memory");
-            if (v >= 8) break;
+          const uint64_t t0 = ptx::globaltimer_ns();
+          for (uint32_t n = 1;; ++n) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(my_flag) : "memory");
+            if (v != 0) break;
             __nanosleep(64);
+            if ((n & 1023u) == 0 && ptx::globaltimer_ns() - t0 > (uint64_t)MM_WATCHDOG_NS)
+              ptx::watchdog_fire(29, 0u, 0u, it, t);
           }
+          // the partial was written through the generic proxy; the bulk copy below
+          // reads it through the async proxy
+          asm volatile("fence.proxy.async.global;" ::: "memory");
         }
-        __syncwarp();   // the acquire by lane 0 is made cumulative for the warp
+        __syncwarp();
       }
       const int acc = it & 1;
       ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), (it >> 1) & 1, 24, it, t);
@@ -397,6 +409,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         }
         ptx::mbar_wait(pb, 0, 28, it, t);
         pst = dstp;
+        if (lane == 0) *reinterpret_cast<volatile int*>(my_flag) = 0;   // consumed: re-arm for the next launch
       }
       if (trace && q == 0 && it < 3) g_trace[blockIdx.x][9 + it] = ptx::globaltimer_ns();
       if (trace && q == 0 && it == 0 && rank == 0) g_trace[blockIdx.x][21] = clock64();
@@ -482,11 +495,10 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       }
       if (to_ws) {   // publish: this warp's rows of the partial are in global memory
         __syncwarp();   // orders the other lanes' stores before lane 0's release
-        if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.ws_flag + pair) : "memory");
-      }
-      if (from_ws) {  // consumed: hand the slot back (8 x -1 returns it to 0)
-        __syncwarp();
-        if (lane == 0) atomicSub(p.ws_flag + (pair - 1), 1);
+        if (lane == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.s32 [%0], 1;" ::"l"(p.ws_flag + pair * 8 + (int)rank * 4 + q) : "memory");
+        }
       }
     }
     if (lane == 0) {
@@ -517,32 +529,25 @@ bool make_sf_map(CUtensorMap* m, const void* base, int64_t rows, int kp, int box
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Library-owned stream-K workspace, one per (device, stream), allocated on first
-// use and grown as needed: [npairs][256][256] fp32 partial tiles + npairs flags
-// (zeroed once; the kernel leaves them at zero).  Not touched by data-parallel runs.
-bool stream_k_workspace(cudaStream_t s, int npairs, float** ws, int** flags) {
-  static std::mutex mu;
-  struct Ent { float* ws = nullptr; int* flags = nullptr; int npairs = 0; };
-  static std::map<std::pair<int, cudaStream_t>, Ent> cache;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  Ent& e = cache[{dev, s}];
-  if (e.npairs < npairs) {
-    if (e.ws) cudaFree(e.ws);
-    if (e.flags) cudaFree(e.flags);
-    e.ws = nullptr;
-    e.flags = nullptr;
-    e.npairs = 0;
-    if (cudaMalloc(&e.ws, (size_t)npairs * 256 * 256 * sizeof(float)) != cudaSuccess) return false;
-    if (cudaMalloc(&e.flags, (size_t)npairs * sizeof(int)) != cudaSuccess) return false;
-    if (cudaMemset(e.flags, 0, (size_t)npairs * sizeof(int)) != cudaSuccess) return false;
-    if (cudaDeviceSynchronize() != cudaSuccess) return false;
-    e.npairs = npairs;
-  }
-  *ws = e.ws;
-  *flags = e.flags;
-  return true;
+// Stream-K schedule: opt-in (MM_GEMM_STREAMK=1) when the last wave of tiles would be
+// ragged and there are only a few waves (each pair then finishes at most one tile
+// left by its neighbour).  Measured on q_proj it LOSES (39 vs 26.7 us): each extra
+// work item costs a full TMEM drain plus a 256 KB fp32 partial round trip, more than
+// the ragged wave it removes.  Kept as a tested alternative schedule.
+int pair_grid(const GemmArgs& a, const GemmConfig& cfg) {
+  const int num_tiles = (int)(((a.M + 255) / 256) * ((a.N + 255) / 256));
+  int grid = sm_count() & ~1;
+  if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas & ~1;
+  if (grid > 2 * num_tiles) grid = 2 * num_tiles;
+  return grid;
+}
+bool use_stream_k(const GemmArgs& a, const GemmConfig& cfg) {
+  const char* sk_env = getenv("MM_GEMM_STREAMK");   // read per call (tests switch it)
+  const bool sk_env_on = sk_env && atoi(sk_env) == 1;
+  const int num_tiles = (int)(((a.M + 255) / 256) * ((a.N + 255) / 256));
+  const int npairs = pair_grid(a, cfg) / 2;
+  return sk_env_on && !cfg.no_stream_k && !cfg.no_workspace && a.n_dst == 0 && npairs > 0 &&
+         num_tiles > npairs && num_tiles % npairs != 0 && num_tiles < 4 * npairs;
 }
 
 template <int STAGES, int NP>
@@ -603,23 +608,16 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.ndst = ndst;
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   if (p.num_tiles == 0) return cudaSuccess;
-  int grid = sm_count() & ~1;
-  if (cfg.max_ctas > 0 && cfg.max_ctas < grid) grid = cfg.max_ctas & ~1;
-  if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
-  // Stream-K when the last wave of tiles would be ragged and there are only a few
-  // waves (each pair then finishes at most one tile left by its neighbour).
+  const int grid = pair_grid(a, cfg);
   const int npairs = grid / 2;
-  // Opt-in (MM_GEMM_STREAMK=1): measured on q_proj it LOSES (40.9 vs 29.6 us) -- each
-  // extra work item costs a full TMEM drain plus a 256 KB fp32 partial round trip,
-  // more than the ragged wave it removes.  Kept as a tested alternative schedule.
-  const bool sk_env_on = [] { const char* e = getenv("MM_GEMM_STREAMK"); return e && atoi(e) == 1; }();
-  p.stream_k = (sk_env_on && !cfg.no_stream_k && p.num_tiles > npairs && p.num_tiles % npairs != 0 &&
-                p.num_tiles < 4 * npairs) ? 1 : 0;
-  if (p.stream_k) {
-    if (!stream_k_workspace(s, npairs, &p.ws, &p.ws_flag)) {
-      *err = "stream-K workspace allocation failed";
-      return cudaErrorMemoryAllocation;
+  p.stream_k = use_stream_k(a, cfg) ? 1 : 0;
+  if (p.stream_k) {   // caller workspace: [flags npairs x 8 ints, 256-B padded][partials]
+    if (!a.ws || a.ws_bytes < pair_workspace_bytes(a, cfg)) {
+      *err = "stream-K workspace missing or too small";
+      return cudaErrorInvalidValue;
     }
+    p.ws_flag = static_cast<int*>(a.ws);
+    p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a.ws) + ws_align((size_t)npairs * 8 * sizeof(int)));
   }
   const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + epi_bytes<STAGES>() + (2 * STAGES + 10) * 8 + 16;
   auto kern = mixgemm2_kernel<STAGES, NP>;
@@ -640,6 +638,12 @@ extern "C" int mm_debug_gemm_trace(unsigned long long* h, int n) {
 }
 
 namespace mmx {
+
+size_t pair_workspace_bytes(const GemmArgs& a, const GemmConfig& cfg) {
+  if (!use_stream_k(a, cfg)) return 0;
+  const size_t npairs = (size_t)(pair_grid(a, cfg) / 2);
+  return ws_align(npairs * 8 * sizeof(int)) + npairs * 256 * 256 * sizeof(float);
+}
 
 cudaError_t launch_mixed_gemm_2cta(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
                                    const char** err) {

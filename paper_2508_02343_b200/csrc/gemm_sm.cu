@@ -286,32 +286,36 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
   if (warp == 2) ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
 }
 
-// Library-owned split-K workspace + counters per (device, stream), grown on demand;
-// counters zeroed once (the kernel re-arms them).
-bool sm_workspace(cudaStream_t s, size_t ws_bytes, int ncnt, float** ws, int** cnt) {
-  static std::mutex mu;
-  struct Ent { float* ws = nullptr; int* cnt = nullptr; size_t bytes = 0; int ncnt = 0; };
-  static std::map<std::pair<int, cudaStream_t>, Ent> cache;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  Ent& e = cache[{dev, s}];
-  if (e.bytes < ws_bytes || e.ncnt < ncnt) {
-    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
-    if (e.ws) cudaFree(e.ws);
-    if (e.cnt) cudaFree(e.cnt);
-    e = Ent{};
-    if (cudaMalloc(&e.ws, ws_bytes) != cudaSuccess) return false;
-    if (cudaMalloc(&e.cnt, (size_t)ncnt * sizeof(int)) != cudaSuccess) return false;
-    if (cudaMemset(e.cnt, 0, (size_t)ncnt * sizeof(int)) != cudaSuccess) return false;
-    if (cudaDeviceSynchronize() != cudaSuccess) return false;
-    e.bytes = ws_bytes;
-    e.ncnt = ncnt;
-  }
-  *ws = e.ws;
-  *cnt = e.cnt;
-  return true;
+// Split count of the small-M kernel: fill the SMs once (one CTA per SM), at least 2
+// stages per unit, at most kMaxSplits (the last unit's reduction reads splits x M x
+// 512 B per tile).
+int sm_splits(const GemmArgs& a, const GemmConfig& cfg) {
+  const int num_nt = (int)((a.N + 127) / 128);
+  int S = (a.geom.kp[0] + 255) / 256 + a.geom.kp[1] / 128 + a.geom.kp[2] / 128;
+  const int sms = cfg.max_ctas > 0 ? cfg.max_ctas : sm_count();
+  int splits = num_nt > 0 ? sms / num_nt : 1;
+  static const int env_splits = [] { const char* e = getenv("MM_GEMM_SPLITS"); return e ? atoi(e) : 0; }();
+  if (env_splits > 0) splits = env_splits;
+  if (splits > S / 2) splits = S / 2;
+  if (splits > kMaxSplits) splits = kMaxSplits;
+  if (splits < 1) splits = 1;
+  return splits;
 }
+int sm_bnm(int64_t M) { return M <= 32 ? 32 : (M <= 64 ? 64 : 128); }
+
+}  // namespace
+
+// Caller workspace of the small-M kernel: [arrival counters: one int per 128-row W
+// tile, 256-B padded][FP32 partials: tiles x splits x BNM x 128].  Zero-filled once by
+// the caller; the last unit of a tile re-arms its counter.
+size_t smallm_workspace_bytes(const GemmArgs& a, const GemmConfig& cfg) {
+  const int splits = sm_splits(a, cfg);
+  if (splits <= 1) return 0;
+  const size_t num_nt = (size_t)((a.N + 127) / 128);
+  return ws_align(num_nt * sizeof(int)) + num_nt * splits * sm_bnm(a.M) * 128 * sizeof(float);
+}
+
+namespace {
 
 template <int BNM, int STAGES>
 cudaError_t run_sm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches, const char** err) {
@@ -349,22 +353,14 @@ cudaError_t run_sm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   { const char* e = getenv("MM_GEMM_SPLIT_INTERLEAVE"); p.interleave = e ? atoi(e) : 0; }
   if (p.num_nt == 0 || a.M == 0) return cudaSuccess;
-  // splits: fill the SMs once (one CTA per SM), at least 2 stages per unit, at most
-  // kMaxSplits (the last unit's reduction reads splits x M x 512 B per tile)
-  const int sms = cfg.max_ctas > 0 ? cfg.max_ctas : sm_count();
-  int splits = sms / p.num_nt;
-  static const int env_splits = [] { const char* e = getenv("MM_GEMM_SPLITS"); return e ? atoi(e) : 0; }();
-  if (env_splits > 0) splits = env_splits;
-  if (splits > S / 2) splits = S / 2;
-  if (splits > kMaxSplits) splits = kMaxSplits;
-  if (splits < 1) splits = 1;
+  (void)S;
+  const int splits = sm_splits(a, cfg);
   p.splits = splits;
-  if (splits > 1) {
-    const size_t ws_bytes = (size_t)p.num_nt * splits * BNM * 128 * sizeof(float);
-    if (!sm_workspace(s, ws_bytes, p.num_nt, &p.ws, &p.cnt)) {
-      *err = "split-K workspace allocation failed";
-      return cudaErrorMemoryAllocation;
-    }
+  if (splits > 1) {   // caller workspace (size checked by the API layer before any launch)
+    const size_t need = smallm_workspace_bytes(a, cfg);
+    if (!a.ws || a.ws_bytes < need) { *err = "split-K workspace missing or too small"; return cudaErrorInvalidValue; }
+    p.cnt = static_cast<int*>(a.ws);
+    p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a.ws) + ws_align((size_t)p.num_nt * sizeof(int)));
   }
   const size_t smem = 1024 + (size_t)STAGES * C::STAGE_BYTES + (2 * STAGES + 1) * 8 + 16;
   auto kern = mixgemm_sm_kernel<BNM, STAGES>;
@@ -380,6 +376,7 @@ cudaError_t run_sm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int
 
 cudaError_t launch_mixed_gemm_smallm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64_t* launches,
                                      const char** err) {
+  // (BNM as in sm_bnm)
   if (a.M <= 32) return run_sm<32, 8>(a, cfg, s, launches, err);
   if (a.M <= 64) return run_sm<64, 8>(a, cfg, s, launches, err);
   return run_sm<128, 6>(a, cfg, s, launches, err);

@@ -73,6 +73,10 @@ struct GemmArgs {
   int n_dst = 0;
   uint16_t* y_dst[8] = {};
   int64_t y_col_off = 0;
+  // Caller-owned GEMM workspace (split-K partials / stream-K partials + flags),
+  // zero-filled before its first use; the kernels leave every counter at zero.
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
 };
 constexpr int kMaxPeers = 8;
 
@@ -81,12 +85,18 @@ struct GemmConfig {
   int num_stages = 0;   // 0 = auto
   int max_ctas = 0;     // 0 = #SMs
   bool no_stream_k = false;  // keep the data-parallel tiling (N-shard path: shard-independent results)
+  bool no_workspace = false; // never pick a path that needs the workspace (N-shard entry points)
   int cluster_pairs = 0;     // CTA-pair GEMM: pairs per cluster (1, 2; 0 = default / MM_GEMM_CP)
 };
 
 // Mixed block-scaled GEMM (gemm.cu).
 cudaError_t launch_mixed_gemm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s,
                               int64_t* launches, const char** err);
+// Workspace bytes the launch of `a` under `cfg` needs (0: none); the per-kernel parts.
+size_t gemm_workspace_bytes(const GemmArgs& a, const GemmConfig& cfg);
+size_t smallm_workspace_bytes(const GemmArgs& a, const GemmConfig& cfg);
+size_t pair_workspace_bytes(const GemmArgs& a, const GemmConfig& cfg);
+constexpr size_t ws_align(size_t b) { return (b + 255) / 256 * 256; }
 
 // [G][M][Ns] -> [M][G*Ns] layout fix after the all-gather (comm.cu).
 cudaError_t launch_gather_layout(const uint16_t* stage, int G, int64_t M, int64_t Ns,
@@ -97,8 +107,9 @@ cudaError_t launch_gather_layout(const uint16_t* stage, int G, int64_t M, int64_
 struct PeerFlags {
   uint32_t* f[kMaxPeers];
 };
-cudaError_t launch_peer_barrier(const PeerFlags& fl, int rank, int world, uint32_t epoch, cudaStream_t s,
-                                int64_t* launches);
+constexpr int kPeerErrSlot = 63;   // flag-array word holding a barrier timeout (missing rank + 1)
+cudaError_t launch_peer_barrier(const PeerFlags& fl, int rank, int world, uint32_t epoch, uint64_t timeout_ns,
+                                cudaStream_t s, int64_t* launches);
 
 int sm_count();
 

@@ -243,7 +243,7 @@ using namespace mmx;
 
 extern "C" {
 
-int32_t mm_abi_version(void) { return 1; }
+int32_t mm_abi_version(void) { return 2; }   // 2: caller GEMM workspace, N-shard stage bytes, peer timeout
 const char* mm_last_error(void) { return g_err.c_str(); }
 int64_t mm_launch_count(void) { return g_launches; }
 void mm_reset_launch_count(void) { g_launches = 0; }
@@ -483,13 +483,21 @@ struct MmPeerWin {
   uint32_t* flags[kMaxPeers] = {};
   void* ipc_base[kMaxPeers] = {};   // mappings opened by mm_peer_window_open (unmapped on close)
   uint32_t epoch = 0;
+  uint64_t timeout_ns = 0;   // 0: the barrier waits forever (mm_peer_window_set_timeout)
 };
 
 static size_t peer_y_bytes(int64_t M, int64_t ldy) { return ((size_t)M * (size_t)ldy * 2 + 255) / 256 * 256; }
 
+static GemmConfig current_cfg() {
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  return g_gemm_cfg;
+}
+
+// d_ws / ws_bytes: caller workspace (see mm_gemm_workspace_bytes); no_ws = an entry
+// point without a workspace argument (N-shard): never pick a path that needs one.
 static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const mm_plan* plan, void* d_y,
-                             int64_t ldy, int64_t n_cols, mm_stream_t stream, bool no_stream_k = false,
-                             const MmPeerWin* win = nullptr) {
+                             int64_t ldy, int64_t n_cols, mm_stream_t stream, void* d_ws, size_t ws_bytes,
+                             bool no_ws, const MmPeerWin* win = nullptr) {
   mm_status st = check_device();
   if (st != MM_OK) return st;
   if ((st = validate_plan(plan)) != MM_OK) return st;
@@ -521,12 +529,15 @@ static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const
     for (int r = 0; r < win->world; ++r) ga.y_dst[r] = win->y[r];
     ga.y_col_off = (int64_t)win->rank * N;
   }
-  GemmConfig cfg;
-  {
-    std::lock_guard<std::mutex> lk(g_cfg_mu);
-    cfg = g_gemm_cfg;
-  }
-  cfg.no_stream_k = cfg.no_stream_k || no_stream_k;
+  GemmConfig cfg = current_cfg();
+  cfg.no_stream_k = cfg.no_stream_k || no_ws;
+  cfg.no_workspace = no_ws;
+  const size_t need = gemm_workspace_bytes(ga, cfg);
+  if (need > 0 && (!d_ws || ws_bytes < need || !aligned(d_ws, 256)))
+    return fail(MM_ERR_WORKSPACE, "GEMM workspace: need %zu bytes (256-B aligned, zero-filled once), got %zu at %p",
+                need, ws_bytes, d_ws);
+  ga.ws = d_ws;
+  ga.ws_bytes = ws_bytes;
   const char* err = "";
   cudaError_t e = launch_mixed_gemm(ga, cfg, reinterpret_cast<cudaStream_t>(stream), &g_launches, &err);
   if (e != cudaSuccess) return fail(MM_ERR_CUDA, "mixed GEMM launch: %s (%s)", cudaGetErrorString(e), err);
@@ -534,8 +545,17 @@ static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const
 }
 
 mm_status mm_mixed_gemm_bf16(const mm_mx_tensor* a, const mm_mx_tensor* w, const mm_plan* plan, void* d_y,
-                             int64_t ldy, mm_stream_t stream) {
-  return gemm_common(a, w, plan, d_y, ldy, w ? w->rows : 0, stream);
+                             int64_t ldy, void* d_ws, size_t ws_bytes, mm_stream_t stream) {
+  return gemm_common(a, w, plan, d_y, ldy, w ? w->rows : 0, stream, d_ws, ws_bytes, false);
+}
+
+int64_t mm_gemm_workspace_bytes(const mm_plan* plan, int64_t M, int64_t N) {
+  if (validate_plan(plan) != MM_OK || M < 0 || N < 0) return -1;
+  GemmArgs ga{};
+  ga.M = M;
+  ga.N = N;
+  ga.geom = geom_of(plan);
+  return (int64_t)gemm_workspace_bytes(ga, current_cfg());
 }
 
 // ---------------------------------------------------------------- multi-GPU
@@ -585,23 +605,29 @@ mm_status mm_comm_destroy(void* comm) {
 
 mm_status mm_mixed_gemm_bf16_nshard_allgather(const mm_mx_tensor* a, const mm_mx_tensor* w_shard,
                                               const mm_plan* plan, int64_t n_total, void* d_y_full, int64_t ldy,
-                                              void* d_stage, void* comm, mm_stream_t stream) {
+                                              void* d_stage, size_t stage_bytes, void* comm, mm_stream_t stream) {
   if (!comm || !d_stage || !a || !w_shard) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
   MmComm* c = static_cast<MmComm*>(comm);
   const int64_t Ns = w_shard->rows;
+  const int64_t M = a->rows;
+  // every precondition is checked before anything is enqueued (the GEMM included)
   if (Ns * c->world != n_total) return fail(MM_ERR_SHAPE, "shard rows * world != n_total");
   if (Ns % 16 != 0) return fail(MM_ERR_SHAPE, "shard rows must be a multiple of 16");
   if (ldy < n_total || ldy % 8 != 0) return fail(MM_ERR_SHAPE, "bad ldy");
   if (!aligned(d_stage, 16)) return fail(MM_ERR_ALIGNMENT, "stage must be 16-byte aligned");
-  const int64_t M = a->rows;
+  if (M > 0 && n_total > 0 && (!d_y_full || !aligned(d_y_full, 16)))
+    return fail(MM_ERR_ALIGNMENT, "Y must be non-NULL and 16-byte aligned");
+  if (M > 0 && stage_bytes < (size_t)M * (size_t)n_total * 2)
+    return fail(MM_ERR_WORKSPACE, "stage: need %lld bytes (BF16 [G][M][N/G]), got %zu",
+                (long long)(M * n_total * 2), stage_bytes);
+  const NcclApi& api = nccl();
+  if (!api.ok) return fail(MM_ERR_NCCL, "libnccl.so.2 could not be loaded");
   uint16_t* stage = static_cast<uint16_t*>(d_stage);
   uint16_t* mine = stage + (int64_t)c->rank * M * Ns;
-  mm_status st = gemm_common(a, w_shard, plan, mine, Ns, Ns, stream, /*no_stream_k=*/true);
+  mm_status st = gemm_common(a, w_shard, plan, mine, Ns, Ns, stream, nullptr, 0, /*no_ws=*/true);
   if (st != MM_OK) return st;
   if (M == 0 || Ns == 0) return MM_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const NcclApi& api = nccl();
-  if (!api.ok) return fail(MM_ERR_NCCL, "libnccl.so.2 could not be loaded");
   ncclResult_t r = api.allGather(mine, stage, (size_t)(M * Ns), ncclBfloat16, c->comm, s);
   if (r != ncclSuccess) return fail(MM_ERR_NCCL, "ncclAllGather: %s", api.errStr(r));
   cudaError_t e = launch_gather_layout(stage, c->world, M, Ns, static_cast<uint16_t*>(d_y_full), ldy, s, &g_launches);
@@ -722,8 +748,25 @@ mm_status mm_peer_barrier(void* win, mm_stream_t stream) {
   PeerFlags fl{};
   for (int r = 0; r < w->world; ++r) fl.f[r] = w->flags[r];
   const uint32_t epoch = ++w->epoch;
-  cudaError_t e = launch_peer_barrier(fl, w->rank, w->world, epoch, reinterpret_cast<cudaStream_t>(stream), &g_launches);
+  cudaError_t e = launch_peer_barrier(fl, w->rank, w->world, epoch, w->timeout_ns,
+                                      reinterpret_cast<cudaStream_t>(stream), &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "peer barrier launch");
+  return MM_OK;
+}
+
+mm_status mm_peer_window_set_timeout(void* win, double seconds) {
+  if (!win || !(seconds >= 0.0)) return fail(MM_ERR_INVALID_ARGUMENT, "NULL window or negative timeout");
+  static_cast<MmPeerWin*>(win)->timeout_ns = (uint64_t)(seconds * 1e9);
+  return MM_OK;
+}
+
+mm_status mm_peer_window_error(void* win, int32_t* h_missing_rank) {
+  if (!win || !h_missing_rank) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  MmPeerWin* w = static_cast<MmPeerWin*>(win);
+  uint32_t v = 0;
+  cudaError_t e = cudaMemcpy(&v, w->flags[w->rank] + kPeerErrSlot, sizeof(v), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "reading the peer error word");
+  *h_missing_rank = (int32_t)v - 1;
   return MM_OK;
 }
 
@@ -738,7 +781,7 @@ mm_status mm_mixed_gemm_bf16_nshard_peerstore(const mm_mx_tensor* a, const mm_mx
   if (a->rows != w->M) return fail(MM_ERR_SHAPE, "activation rows %lld != window M %lld", (long long)a->rows, (long long)w->M);
   if (w->ldy < n_total) return fail(MM_ERR_SHAPE, "window ldy < n_total");
   mm_status st = gemm_common(a, w_shard, plan, w->y[w->rank] + (int64_t)w->rank * Ns, w->ldy, Ns, stream,
-                             /*no_stream_k=*/true, w);
+                             nullptr, 0, /*no_ws=*/true, w);
   if (st != MM_OK) return st;
   if (barrier) return mm_peer_barrier(win, stream);
   return MM_OK;

@@ -32,7 +32,7 @@ def test_header_matches_binding_list():
 def test_library_exports_every_symbol(L):
     for name in _header_symbols():
         assert hasattr(L, name), name
-    assert L.mm_abi_version() == 1
+    assert L.mm_abi_version() == 2
 
 
 def _plan(K, n, fmt6=mm.MM_E3M2, fmt8=mm.MM_E4M3):
