@@ -5,11 +5,20 @@ A STEP is one pass of the whole hot path over one batch of synthetic input:
     mm_mixed_gemm_bf16(A, W)    (3-segment block-scaled tcgen05 GEMM, rows R7-R8)
 against offline-calibrated, offline-quantized weights (rows R0, R6; untimed).
 
-Default workload (BASELINE.json configs[1]): Llama-3.1-8B q_proj, M=2048 K=4096
-N=4096, calibrated plan, 1 GPU.  At N>1 GPUs every rank runs its own batch through
-the same layer (data-parallel replicas, weak scaling, no collective);
-`--config llama70b_down` instead N-shards the 70B down_proj over the ranks with
-the library's NCCL all-gather of the BF16 outputs (strong scaling).
+Default workload at N=1 (BASELINE.json configs[1]): Llama-3.1-8B q_proj, M=2048
+K=4096 N=4096, calibrated plan.  Default at N>1 (BASELINE.json configs[3], the
+north star's multi-GPU case): the Llama-3.1-70B down_proj (M=8192 K=28672 N=8192)
+N-sharded over the N ranks -- each rank quantizes the replicated activation and
+computes its N/G output channels, and the library's NCCL all-gather assembles the
+BF16 Y on every rank (strong scaling); the fused all-gather epilogue (peer stores
+over NVLink) is timed on the same ranks and reported in `fused_allgather`.
+`--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N local ranks (127.0.0.1 rendezvous).
+
+Timing: the K timed steps run back to back, split into R = min(5, K) chunks with
+one CUDA event between chunks; `value`/`ms_per_step` come from the whole region,
+`ms_per_step_stats` gives the median / p10 / p90 over the chunks.  Per-kernel
+durations: R passes of K back-to-back launches of that kernel alone.
 
 L2 policy: every step reads a different one of `nsets` rotating input sets
 (activations, quantized weights, outputs) whose total exceeds 2x the 126 MB L2,
@@ -75,6 +84,34 @@ def rq_bytes(M, n):
     """Algorithmic reorder-quantize bytes: BF16 read + packed codes + E8M0 scales (no padding)."""
     K = sum(n)
     return 2 * M * K + M * (n[0] // 2 + 3 * n[1] // 4 + n[2]) + M * K // 32
+
+
+def host_facts():
+    """CPU model, sockets and usable threads of this host (for cpu_baseline)."""
+    model, sockets = None, set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name") and model is None:
+                    model = line.split(":", 1)[1].strip()
+                elif line.startswith("physical id"):
+                    sockets.add(line.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = os.cpu_count()
+    return {"cpu_model": model, "sockets": max(1, len(sockets)), "cpu_count": os.cpu_count(),
+            "usable_threads": usable}
+
+
+def pct(vals, q):
+    return float(np.percentile(np.asarray(vals, dtype=np.float64), q)) if vals else None
+
+
+def stats(vals):
+    return {"median": pct(vals, 50), "p10": pct(vals, 10), "p90": pct(vals, 90), "n": len(vals)}
 
 
 class ClockSampler:
@@ -155,21 +192,51 @@ def max_over_ranks(v: float, world: int) -> float:
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) arm
-def oracle_cpu_rate(M, K, N, budget_s=15.0, seed_layer=0):
+def calib_rows_for(K):
+    """Calibration rows of BOTH arms (the GPU arm's plan and the oracle's are equal)."""
+    return 16384 if K <= 8192 else 2048
+
+
+_ORACLE_PLAN = {}
+
+
+def oracle_plan(K, seed_layer=0):
+    """The oracle's calibration of the same calibration draw the GPU arm uses."""
+    from oracle import calib as ocal
+    from synth import bf16_bits, gen_act
+    key = (K, seed_layer)
+    if key not in _ORACLE_PLAN:
+        cal = ocal.calibrate(bf16_bits(gen_act(calib_rows_for(K), K, 1000 + seed_layer, 2000 + 10 * seed_layer)))
+        _ORACLE_PLAN[key] = (cal["perm"], cal["n"])
+    return _ORACLE_PLAN[key]
+
+
+def oracle_cpu_rate(M, K, N, budget_s=15.0, seed_layer=0, threads=None):
     """Time the CPU oracle (as it stands) on a bounded row sample of the workload:
     reorder-quantize of the sampled activation rows + fp64 GEMM of the dequantized
     operands against all N output channels.  The weight quantization is offline for
-    both arms and is done before timing.  Returns (TFLOP/s, sample text, threads, rows/s)."""
-    from oracle import calib as ocal
+    both arms and is done before timing.  threads=1 limits BLAS and OpenMP to one
+    thread.  Returns (TFLOP/s, sample text, threads used, rows/s, n4_n6_n8)."""
+    import contextlib
+
     from oracle import mx as omx
     from synth import bf16_bits, gen_act, gen_weight
+    perm, n = oracle_plan(K, seed_layer)
+    omx.encode(np.zeros(1), 0)            # load the OpenMP encoder so threadpoolctl sees it
     try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        from threadpoolctl import threadpool_info, threadpool_limits
+        ctx = threadpool_limits(limits=threads) if threads else contextlib.nullcontext()
     except Exception:
-        threads = os.cpu_count()
-    cal = ocal.calibrate(bf16_bits(gen_act(2048 if K <= 8192 else 512, K, 1000 + seed_layer, 2000)))
-    perm, n = cal["perm"], cal["n"]
+        threadpool_info, ctx = None, contextlib.nullcontext()
+    with ctx:
+        try:
+            used = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        except Exception:
+            used = threads or os.cpu_count()
+        return _oracle_loop(M, K, N, budget_s, seed_layer, perm, n, omx, bf16_bits, gen_act, gen_weight) + (used, n)
+
+
+def _oracle_loop(M, K, N, budget_s, seed_layer, perm, n, omx, bf16_bits, gen_act, gen_weight):
     w_bits = bf16_bits(gen_weight(N, K, 3000 + seed_layer))
     wc, wsf, _ = omx.reorder_quantize(w_bits, perm, n)
     Wd = omx.dequantize_segments(wc, wsf)
@@ -189,7 +256,7 @@ def oracle_cpu_rate(M, K, N, budget_s=15.0, seed_layer=0):
     tflops = 2.0 * total_rows * N * K / t_total / 1e12
     sample = (f"{total_rows} activation rows ({total_rows / M:.2f} x the M={M} batch; reorder-quantize + fp64 "
               f"GEMM vs all {N} channels) in {t_total:.1f} s; weights quantized offline (untimed)")
-    return tflops, sample, threads, total_rows / t_total
+    return tflops, sample, total_rows / t_total
 
 
 def run_reference(args, rank, world):
@@ -200,17 +267,21 @@ def run_reference(args, rank, world):
     sample = ""
     threads = 1
     per = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    n = None
     for i in range(args.warmup + args.steps):
-        v, sample, threads, _ = oracle_cpu_rate(M, K, N, budget_s=per)
+        v, sample, _, threads, n = oracle_cpu_rate(M, K, N, budget_s=per)
         if i >= args.warmup:
             vals.append(v)
     v = statistics.median(vals)
     ms = 2.0 * M * N * K / (v * 1e12) * 1e3
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": text, "M": M, "K": K, "N": N},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+           "scaling": "strong" if world > 1 and args.config == "llama70b_down" else "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": text, "M": M, "K": K, "N": N, "n4_n6_n8": [int(c) for c in n],
+                      "calibration_rows": calib_rows_for(K)},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                            "host": host_facts(), "per_step_tflops": stats(vals)},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -221,7 +292,9 @@ def build_layer(M, K, N, n_sets, device, layer=0, calib_rows=16384, n_shard=None
     distinct weight matrices, allocate n_sets activation / output buffers."""
     import paper_2508_02343_b200 as mm
     from synth import gen_act, gen_weight
-    cal_x = gen_act(calib_rows, K, 1000 + layer, 2000 + 10 * layer, device=device)
+    # calibration draw generated on the host (the oracle arm calibrates on the very same
+    # BF16 rows, so both arms quantize with the same plan)
+    cal_x = gen_act(calib_rows, K, 1000 + layer, 2000 + 10 * layer).to(device)
     plan = mm.mm_calibrate_thresholds(cal_x)
     del cal_x
     Ns = N if n_shard is None else N // world
@@ -240,6 +313,67 @@ def build_layer(M, K, N, n_sets, device, layer=0, calib_rows=16384, n_shard=None
     return plan, sets
 
 
+def timed_chunks(stream, n_steps, fn, sleep_ms):
+    """n_steps calls of fn(i) back to back on `stream`, split into R = min(5, n_steps)
+    chunks with one event between chunks, pre-queued behind a device sleep so the
+    events time device execution.  Returns (total ms, [ms per step of each chunk])."""
+    R = max(1, min(5, n_steps))
+    bounds = [round(j * n_steps / R) for j in range(R + 1)]
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(R + 1)]
+    torch.cuda._sleep(int(sleep_ms * 1e-3 * 1.9e9))
+    evs[0].record(stream)
+    for j in range(R):
+        for i in range(bounds[j], bounds[j + 1]):
+            fn(i)
+        evs[j + 1].record(stream)
+    torch.cuda.synchronize()
+    per = [evs[j].elapsed_time(evs[j + 1]) / max(1, bounds[j + 1] - bounds[j]) for j in range(R)]
+    return evs[0].elapsed_time(evs[R]), per
+
+
+def kernel_passes(stream, steps, fn, reps=5):
+    """`reps` passes of `steps` back-to-back launches of ONE kernel (fn(i)), each
+    bracketed by two events -> average launch duration per pass (ms)."""
+    out = []
+    for _ in range(reps):
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(int(min(400.0, 1.0 + 0.2 * steps) * 1e-3 * 1.9e9))
+        k0.record(stream)
+        for i in range(steps):
+            fn(i)
+        k1.record(stream)
+        torch.cuda.synchronize()
+        out.append(k0.elapsed_time(k1) / steps)
+    return out
+
+
+def measure_shape(M, K, N, dev, stream, pk, launches=10, layer=0):
+    """Extra driver-observed single-GPU shape: RQ and GEMM alone, 5 passes of
+    `launches` back-to-back launches over 2 rotating sets (each set > L2)."""
+    import paper_2508_02343_b200 as mm
+    plan, sets = build_layer(M, K, N, 2, dev, layer=layer, calib_rows=calib_rows_for(K))
+    with torch.cuda.stream(stream):
+        for st in sets:
+            mm.mm_reorder_quantize_act(st["x"], plan, out=st["a"], stream=stream)
+            mm.mm_mixed_gemm_bf16(st["a"], st["wq"], plan, out=st["y"], stream=stream)
+        torch.cuda.synchronize()
+        rq = kernel_passes(stream, launches, lambda i: mm.mm_reorder_quantize_act(
+            sets[i % 2]["x"], plan, out=sets[i % 2]["a"], stream=stream))
+        gm = kernel_passes(stream, launches, lambda i: mm.mm_mixed_gemm_bf16(
+            sets[i % 2]["a"], sets[i % 2]["wq"], plan, out=sets[i % 2]["y"], stream=stream))
+    n = plan.n
+    rq_ms, gm_ms = statistics.median(rq), statistics.median(gm)
+    rq_gbs = rq_bytes(M, n) / (rq_ms * 1e-3) / 1e9
+    tf = 2.0 * M * N * K / (gm_ms * 1e-3) / 1e12
+    pmix = mix_peak_tflops(n, pk)
+    del sets
+    torch.cuda.empty_cache()
+    return {"M": M, "K": K, "N": N, "n4_n6_n8": list(n), "rq_us": rq_ms * 1e3, "rq_gbs": rq_gbs,
+            "rq_frac_hbm": rq_gbs / pk["hbm_gbs"], "gemm_us": gm_ms * 1e3, "gemm_tflops": tf,
+            "gemm_frac_mix_peak": tf / pmix, "rq_us_stats": stats([v * 1e3 for v in rq]),
+            "gemm_us_stats": stats([v * 1e3 for v in gm])}
+
+
 def run_gpu(args, rank, world, local):
     import paper_2508_02343_b200 as mm
     M, K, N, text = CONFIGS[args.config]
@@ -248,11 +382,14 @@ def run_gpu(args, rank, world, local):
         mm.mm_set_gemm_config(args.gemm_bn, args.gemm_stages, 0)
     pk = peaks()
     nshard = args.config == "llama70b_down" and (world > 1 or args.comm == "peer")
+    use_peer = nshard and args.comm == "peer"
     comm = win = y_peer = None
-    if nshard and args.comm == "nccl":
+    if nshard:
         from paper_2508_02343_b200.dist import exchange_unique_id
-        comm = mm.mm_comm_init(rank, world, exchange_unique_id(mm.nccl_unique_id))
-    elif nshard:   # fused all-gather epilogue: tiles stored into every rank's Y over NVLink
+        comm = mm.mm_comm_init(rank, world, exchange_unique_id(mm.nccl_unique_id)) if world > 1 else \
+            mm.mm_comm_init(0, 1, mm.nccl_unique_id())
+    if nshard and (use_peer or (world > 1 and not args.no_fused)):
+        # fused all-gather epilogue: tiles stored into every rank's Y over NVLink
         if world > 1:
             from paper_2508_02343_b200.dist import open_peer_window
             win, y_peer = open_peer_window(M, N)
@@ -261,19 +398,19 @@ def run_gpu(args, rank, world, local):
             win, y_peer = mm.PeerWindow.from_ptrs(0, 1, [buf], M, N), mm.peer_y(buf, M, N)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     # bytes touched per step (for the L2 rotation count)
-    per_set = 2 * M * K + M * K + (N // world if nshard else N) * K + 2 * M * N
+    Ns = N // world if nshard else N
+    per_set = 2 * M * K + M * K + Ns * K + 2 * M * N
     n_sets = max(2, min(16, -(-3 * l2 // per_set)))
     if args.config == "cfg1":
         n_sets = 2
     plan, sets = build_layer(M, K, N, n_sets, dev, n_shard=(True if nshard else None), rank=rank, world=world,
-                             calib_rows=16384 if K <= 8192 else 2048)
+                             calib_rows=calib_rows_for(K))
     n = plan.n
     stage = torch.empty(M * N, dtype=torch.bfloat16, device=dev) if nshard else None
     stream = torch.cuda.Stream(dev)
-    Ns = N // world if nshard else N
 
-    def gemm(st, y=None):
-        if nshard and win is not None:
+    def gemm(st, y=None, peer=use_peer):
+        if nshard and peer:
             mm.mm_mixed_gemm_bf16_nshard_peerstore(st["a"], st["wq"], plan, N, win, barrier=True, stream=stream)
         elif nshard:
             mm.mm_mixed_gemm_bf16_nshard_allgather(st["a"], st["wq"], plan, N, comm, out=st["y"] if y is None else y,
@@ -281,17 +418,12 @@ def run_gpu(args, rank, world, local):
         else:
             mm.mm_mixed_gemm_bf16(st["a"], st["wq"], plan, out=st["y"] if y is None else y, stream=stream)
 
-    def step(i, evs=None):
+    def step(i, peer=use_peer):
         s = sets[i % n_sets]
-        if evs is not None:
-            evs[0].record(stream)
         mm.mm_reorder_quantize_act(s["x"], plan, out=s["a"], stream=stream)
-        if evs is not None:
-            evs[1].record(stream)
-        gemm(s)
-        if evs is not None:
-            evs[2].record(stream)
+        gemm(s, peer=peer)
 
+    sleep_ms = min(400.0, 1.0 + 0.3 * args.steps) * (20.0 if nshard else 1.0)
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
             step(i)
@@ -307,43 +439,63 @@ def run_gpu(args, rank, world, local):
             if i % 64 == 0:
                 stream.synchronize()
         stream.synchronize()
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier(world)
         torch.cuda.synchronize()
         l0 = mm.launch_count()
-        # pre-queue a device sleep so the host enqueues all K steps while the GPU is
-        # busy: the events below then time back-to-back device execution only
-        # (host enqueue cost is what the e2e number includes).  Only the two
-        # boundary events sit in the stream, so consecutive kernels keep their
-        # programmatic-dependent-launch overlap.
-        torch.cuda._sleep(int(min(400.0, 1.0 + 0.3 * args.steps) * 1e-3 * 1.9e9))
-        t0.record(stream)
-        for i in range(args.steps):
-            step(i)
-        t1.record(stream)
-        torch.cuda.synchronize()
+        # K steps back to back (only chunk-boundary events in the stream, so consecutive
+        # kernels keep their programmatic-dependent-launch overlap)
+        total_ms, chunk_ms = timed_chunks(stream, args.steps, step, min(400.0, sleep_ms))
         barrier(world)
         launches = mm.launch_count() - l0
-        # per-kernel passes: K back-to-back launches of ONE kernel over the same
-        # rotation, bracketed by two events -> that kernel's average launch duration
-        def kernel_pass(fn):
-            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda._sleep(int(min(400.0, 1.0 + 0.2 * args.steps) * 1e-3 * 1.9e9))
-            k0.record(stream)
-            for i in range(args.steps):
-                fn(sets[i % n_sets])
-            k1.record(stream)
-            torch.cuda.synchronize()
-            return k0.elapsed_time(k1) / args.steps
-        rq_ms = kernel_pass(lambda st: mm.mm_reorder_quantize_act(st["x"], plan, out=st["a"], stream=stream))
-        gemm_ms = kernel_pass(gemm)
+        # per-kernel passes: that kernel's average launch duration over the same rotation
+        rq_pass = kernel_passes(stream, args.steps, lambda i: mm.mm_reorder_quantize_act(
+            sets[i % n_sets]["x"], plan, out=sets[i % n_sets]["a"], stream=stream))
+        gemm_pass = kernel_passes(stream, args.steps, lambda i: gemm(sets[i % n_sets]))
+        extra_nshard = {}
+        if nshard and world > 1:
+            # the N-shard GEMM alone (no exchange) and the bare collective on the same bytes
+            gemm_only = kernel_passes(stream, args.steps, lambda i: mm.mm_mixed_gemm_bf16(
+                sets[i % n_sets]["a"], sets[i % n_sets]["wq"], plan, out=stage[: M * Ns].view(M, Ns), stream=stream))
+            import torch.distributed as dist
+            src = stage[rank * M * Ns:(rank + 1) * M * Ns]
+            ag = []
+            for _ in range(5):
+                barrier(world)
+                e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0_.record(stream)
+                for _i in range(args.steps):
+                    dist.all_gather_into_tensor(stage, src)
+                e1_.record(stream)
+                torch.cuda.synchronize()
+                ag.append(e0_.elapsed_time(e1_) / args.steps)
+            ag_ms = max_over_ranks(statistics.median(ag), world)
+            extra_nshard = {
+                "gemm_shard_us": max_over_ranks(statistics.median(gemm_only), world) * 1e3,
+                "allgather_us": ag_ms * 1e3,
+                "allgather_busbw_gbs": (world - 1) / world * (2 * M * N) / (ag_ms * 1e-3) / 1e9,
+                "allgather_bytes": 2 * M * N,
+                "allgather_note": "torch.distributed all_gather_into_tensor (NCCL) of the same BF16 bytes, "
+                                  "busbw = (G-1)/G x bytes / time"}
+            if win is not None:   # the fused all-gather epilogue on the same ranks
+                barrier(world)
+                torch.cuda.synchronize()
+                f_total, f_chunks = timed_chunks(stream, args.steps, lambda i: step(i, peer=True),
+                                                 min(400.0, sleep_ms))
+                barrier(world)
+                f_ms = max_over_ranks(f_total, world) / args.steps
+                extra_nshard["fused_allgather"] = {
+                    "value": 2.0 * M * N * K / (f_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": f_ms,
+                    "what": "RQ + GEMM with every tile TMA-stored into every rank's Y over peer memory + flag "
+                            "barrier (mm_mixed_gemm_bf16_nshard_peerstore)"}
         clocks = sampler.stop()
-    total_ms = max_over_ranks(t0.elapsed_time(t1), world)
+    total_ms = max_over_ranks(total_ms, world)
     ms = total_ms / args.steps
     flops_rank = 2.0 * M * Ns * K
     units = flops_rank * world * args.steps                       # all ranks' useful FLOPs
     value = units / (total_ms * 1e-3) / 1e12
+    rq_ms, gemm_ms = statistics.median(rq_pass), statistics.median(gemm_pass)
     gemm_tflops = flops_rank / (gemm_ms * 1e-3) / 1e12
+    kpad = sum(plan.padded_cols(g) for g in range(3))
     pmix = mix_peak_tflops(n, pk)
     rqb = rq_bytes(M, n)
     rq_gbs = rqb / (rq_ms * 1e-3) / 1e9
@@ -355,7 +507,7 @@ def run_gpu(args, rank, world, local):
     # the peer-store path has one Y window and runs the steps serially.
     x_host = sets[0]["x"].cpu().pin_memory()
     y_hosts = [torch.empty(M, N, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-    pipelined = y_peer is None
+    pipelined = not use_peer
     slots = [sets[0], sets[1 % n_sets]] if pipelined else [sets[0]]
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "rq", "comp", "out")}
@@ -363,7 +515,7 @@ def run_gpu(args, rank, world, local):
     def e2e_step(i):
         b = i % len(slots)
         st = slots[b]
-        y_dev = y_peer if y_peer is not None else st["y"]
+        y_dev = y_peer if use_peer else st["y"]
         if not pipelined:
             with torch.cuda.stream(stream):
                 st["x"].copy_(x_host, non_blocking=True)
@@ -411,41 +563,67 @@ def run_gpu(args, rank, world, local):
         barrier(world)   # no rank unmaps while a peer may still store into it
         win.close()
 
+    large = None
+    if world == 1 and args.large and args.config == "q_proj":
+        M3, K3, N3 = 16384, 14336, 4096
+        large = measure_shape(M3, K3, N3, dev, stream, pk, layer=1)
+        large["workload"] = "Llama-3.1-8B down_proj at batch 8 x seq 2048 (BASELINE configs[2], b8 down)"
+
     if rank != 0:
         return
     # ---- CPU baseline (oracle as it stands, bounded sample) -----------------------------
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, sample, threads, _ = oracle_cpu_rate(M, K, N, budget_s=args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
+        v, sample, _, threads, _ = oracle_cpu_rate(M, K, N, budget_s=args.cpu_seconds)
+        v1, sample1, _, _, _ = oracle_cpu_rate(M, K, N, budget_s=max(3.0, args.cpu_seconds / 2), threads=1)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+               "host": host_facts(), "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "sample": sample1}}
 
+    traffic_src = None
+    tr = {}
+    if args.traffic:
+        try:
+            with open(os.path.join(ROOT, args.traffic)) as f:
+                tr = json.load(f)
+            traffic_src = (f"{args.traffic}: ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per "
+                           f"launch, captured {tr.get('captured', '?')} at commit {tr.get('commit', '?')} "
+                           f"(static file, not re-measured by this run)")
+        except Exception:
+            tr = {}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if nshard else "weak", "vs_baseline": None,
         "dtype": "mxfp4/mxfp6(e3m2)/mxfp8(e4m3) x e8m0, fp32 accum, bf16 out", "data": "synthetic",
         "config": {"workload": text, "M": M, "K": K, "N": N, "n4_n6_n8": list(n),
-                   "parallelism": ((f"N-shard x{world} + NCCL all-gather" if win is None else
+                   "calibration_rows": calib_rows_for(K),
+                   "parallelism": ((f"N-shard x{world} + NCCL all-gather" if not use_peer else
                                     f"N-shard x{world}, all-gather fused into the GEMM epilogue (peer stores)")
                                    if nshard else
                                    ("replicas" if world > 1 else "1 GPU")),
                    "l2": f"{n_sets} rotating input/weight/output sets, {n_sets * per_set / 1e6:.0f} MB > L2 "
-                         f"{l2 / 1e6:.0f} MB",
+                         f"{l2 / 1e6:.0f} MB (inputs differ from step to step; no L2 flush)",
                    "timing": "CUDA events on the launching stream; steps pre-queued behind a device sleep "
-                             "(device time; host enqueue cost is in e2e); value/ms_per_step from boundary events "
-                             "only; per-kernel durations (breakdown, roofline) = K back-to-back launches of that "
-                             "kernel alone over the same rotation / K"},
+                             "(device time; host enqueue cost is in e2e); value/ms_per_step from the whole region "
+                             "(R <= 5 chunks, one event between chunks); per-kernel durations (breakdown, roofline) "
+                             "= median of 5 passes of K back-to-back launches of that kernel alone"},
+        "ms_per_step_stats": stats(chunk_ms),
         "breakdown": {"rq_us": rq_ms * 1e3, "gemm_us": gemm_ms * 1e3,
+                      "rq_us_stats": stats([v * 1e3 for v in rq_pass]),
+                      "gemm_us_stats": stats([v * 1e3 for v in gemm_pass]),
                       "rq_gbs": rq_gbs, "rq_frac_hbm": rq_gbs / pk["hbm_gbs"],
-                      "gemm_tflops": gemm_tflops, "gemm_mix_peak_tflops": pmix,
+                      "gemm_tflops": gemm_tflops, "gemm_tflops_padded_k": gemm_tflops * kpad / K,
+                      "k_padded": kpad, "gemm_mix_peak_tflops": pmix,
                       "gemm_frac_mix_peak": gemm_tflops / pmix,
                       "peaks": f"{pk['src']}: HBM {pk['hbm_gbs']:.0f} GB/s, bf16 {pk['bf16']:.0f} TF/s "
                                f"(fp8 = 2x, fp4 = 4x)"},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": pmix, "unit": "TFLOP/s",
-                     "frac": gemm_tflops / pmix, "traffic": None,
-                     "kernel": "mixgemm2_kernel (CTA-pair tcgen05; algorithmic 2*M*N*K per launch; mix-weighted MXFP4/FP8 peak)"},
+                     "frac": gemm_tflops / pmix, "traffic": tr.get("mixgemm"), "traffic_source": traffic_src,
+                     "kernel": "mixgemm2_kernel (CTA-pair tcgen05; algorithmic 2*M*N*K per launch; "
+                               "mix-weighted MXFP4/FP8 peak)" + ("; N-shard: GEMM + all-gather + layout" if nshard
+                                                                else "")},
         "rq_roofline": {"bound": "hbm", "achieved": rq_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                        "frac": rq_gbs / pk["hbm_gbs"], "traffic": None,
+                        "frac": rq_gbs / pk["hbm_gbs"], "traffic": tr.get("rq"), "traffic_source": traffic_src,
                         "kernel": "rq_kernel (algorithmic BF16 read + packed codes + scales)"},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 2 * M * K,
                 "d2h_bytes_per_step": 2 * M * N,
@@ -455,16 +633,26 @@ def run_gpu(args, rank, world, local):
         "clocks": clocks,
         "cpu_baseline": cpu,
     }
-    if args.traffic:
-        try:
-            with open(os.path.join(ROOT, args.traffic)) as f:
-                tr = json.load(f)
-            out["roofline"]["traffic"] = tr.get("mixgemm")
-            out["rq_roofline"]["traffic"] = tr.get("rq")
-        except Exception:
-            pass
+    if extra_nshard:
+        out["nshard"] = extra_nshard
+    if large is not None:
+        out["large_shape"] = large
     print(json.dumps(out), flush=True)
 
+
+def relaunch_under_torchrun(n):
+    """`--gpus N` (N > 1) without a torch.distributed environment: run this same
+    command under torch.distributed.run with N local ranks and exit with its code."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")    # NCCL's init log shows the N ranks
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def main():
@@ -473,19 +661,27 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="micromix", choices=["micromix", "reference"])
-    ap.add_argument("--config", default="q_proj", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: q_proj at N=1 (configs[1]), llama70b_down N-shard at N>1 (configs[3])")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
-                    help="N-shard output exchange: NCCL all-gather, or the fused peer-store epilogue")
+                    help="N-shard output exchange of the headline value: NCCL all-gather, or the fused "
+                         "peer-store epilogue")
+    ap.add_argument("--no-fused", action="store_true", help="N>1: skip timing the fused all-gather epilogue")
+    ap.add_argument("--large", type=int, default=1, help="N=1: also time the b8 down_proj shape (1/0)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gemm-bn", type=int, default=0, help="GEMM tile N override (tuning)")
     ap.add_argument("--gemm-stages", type=int, default=0, help="GEMM pipeline stages override (tuning)")
-    ap.add_argument("--traffic", default="profiles/traffic_r01j.json",
+    ap.add_argument("--traffic", default="profiles/traffic_r02.json",
                     help="ncu dram bytes per launch (written from an ncu --set full capture)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        relaunch_under_torchrun(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:
+        args.config = "llama70b_down" if max(world, args.gpus if args.impl == "reference" else 1) > 1 else "q_proj"
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         run_reference(args, rank, world)
