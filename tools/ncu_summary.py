@@ -105,6 +105,14 @@ def main(src, tag):
         md.append("")
     with open(os.path.join(out, f"{tag}_kernels.md"), "w") as f:
         f.write("\n".join(md) + "\n")
+    import datetime
+    import subprocess
+    try:
+        commit = subprocess.check_output(["git", "-C", ROOT, "rev-parse", "--short=12", "HEAD"], text=True).strip()
+    except Exception:
+        commit = None
+    traffic["captured"] = f"{tag} ({datetime.date.today().isoformat()})"
+    traffic["commit"] = commit
     with open(os.path.join(out, f"traffic_{tag}.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     print("\n".join(md))
