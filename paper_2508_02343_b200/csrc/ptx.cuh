@@ -80,10 +80,14 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, i
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag = 0, int a = 0, int b = 0) {
   if (mbar_try_wait(bar, parity)) return;
 #if MM_WATCHDOG_NS
+  // the timer is read once per 1024 polls (an inner loop without it), so the spin
+  // costs two instructions per poll
   const uint64_t t0 = globaltimer_ns();
-  uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > (uint64_t)MM_WATCHDOG_NS) watchdog_fire(tag, bar, parity, a, b);
+  for (;;) {
+#pragma unroll 1
+    for (int n = 0; n < 1024; ++n)
+      if (mbar_try_wait(bar, parity)) return;
+    if (globaltimer_ns() - t0 > (uint64_t)MM_WATCHDOG_NS) watchdog_fire(tag, bar, parity, a, b);
   }
 #else
   while (!mbar_try_wait(bar, parity)) {

@@ -113,6 +113,25 @@ template <> struct Slot<1> { using T = uint16_t; };
 template <> struct Slot<2> { using T = uint32_t; };
 template <> struct Slot<4> { using T = uint2; };
 
+// Shared-memory slot load at a 32-bit shared address (the gather: stage base, a
+// uniform register, + a per-lane table offset -> one LDS [R + UR]).
+template <typename ST> __device__ __forceinline__ ST lds_slot(uint32_t addr);
+template <> __device__ __forceinline__ uint16_t lds_slot<uint16_t>(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+template <> __device__ __forceinline__ uint32_t lds_slot<uint32_t>(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+template <> __device__ __forceinline__ uint2 lds_slot<uint2>(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+
 // Row RHO of a slot as an fp32 value (BF16 = the top half of an fp32).
 template <int RHO>
 __device__ __forceinline__ float slot_f32(const uint16_t& s) { return __uint_as_float(uint32_t(s) << 16); }
@@ -250,7 +269,7 @@ __device__ __forceinline__ void block_amax(const uint16_t (&v)[NV], uint32_t (&a
   uint32_t m = 0;
 #pragma unroll
   for (int i = 0; i < NV; ++i) m = max(m, uint32_t(v[i]) & 0x7FFFu);
-  if constexpr (NV == 16) m = max(m, __shfl_xor_sync(3u << (threadIdx.x & 30), m, 1));
+  if constexpr (NV == 16) m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
   am[0] = m;
 }
 // max(|a|, |b|) per BF16 half (sign = xor of the signs; masked off by the caller):
@@ -277,7 +296,7 @@ __device__ __forceinline__ uint32_t tree_reduce(const uint32_t (&w)[NV], F f) {
 template <int NV>
 __device__ __forceinline__ void block_amax(const uint32_t (&v)[NV], uint32_t (&am)[4]) {
   uint32_t m = tree_reduce<NV>(v, absmax_bf16x2);
-  if constexpr (NV == 16) m = absmax_bf16x2(m, __shfl_xor_sync(3u << (threadIdx.x & 30), m, 1));
+  if constexpr (NV == 16) m = absmax_bf16x2(m, __shfl_xor_sync(0xffffffffu, m, 1));
   am[0] = m & 0x7FFFu;
   am[1] = (m >> 16) & 0x7FFFu;
 }
@@ -288,8 +307,8 @@ __device__ __forceinline__ void block_amax(const uint2 (&v)[NV], uint32_t (&am)[
   for (int i = 0; i < NV; ++i) { x[i] = v[i].x; y[i] = v[i].y; }
   uint32_t m01 = tree_reduce<NV>(x, absmax_bf16x2), m23 = tree_reduce<NV>(y, absmax_bf16x2);
   if constexpr (NV == 16) {
-    m01 = absmax_bf16x2(m01, __shfl_xor_sync(3u << (threadIdx.x & 30), m01, 1));
-    m23 = absmax_bf16x2(m23, __shfl_xor_sync(3u << (threadIdx.x & 30), m23, 1));
+    m01 = absmax_bf16x2(m01, __shfl_xor_sync(0xffffffffu, m01, 1));
+    m23 = absmax_bf16x2(m23, __shfl_xor_sync(0xffffffffu, m23, 1));
   }
   am[0] = m01 & 0x7FFFu;
   am[1] = (m01 >> 16) & 0x7FFFu;
@@ -304,35 +323,46 @@ __device__ __forceinline__ void block_amax(const uint2 (&v)[NV], uint32_t (&am)[
 // packed and stored.
 template <int RHO, int G, int FMT, int NV, typename ST>
 __device__ __forceinline__ void quantize_row(const ST (&v)[NV], uint32_t amax, int off, uint8_t* crow,
-                                             uint8_t* sfp, bool store_codes, bool store_sf) {
+                                             uint8_t* sfp, bool store_codes, bool store_sf, bool zero) {
   const int sb = max(int(amax >> 7) - off, 0);                  // E8M0 byte = e + 127
   const float inv = __uint_as_float(uint32_t(254 - sb) << 23);  // 2^-e exactly
-  if (store_sf) sfp[16 * RHO] = uint8_t(sb);
-  if (store_codes) encode_store<G, FMT, RHO, NV>(v, inv, crow);
+  if (store_sf) sfp[16 * RHO] = zero ? uint8_t(0) : uint8_t(sb);
+  if (store_codes) {
+    if (zero) {   // padding block: zero codes
+      constexpr int hb = G == 0 ? NV / 2 : (G == 1 ? 3 * NV / 4 : NV);
+#pragma unroll
+      for (int b = 0; b < hb; b += 4) *reinterpret_cast<uint32_t*>(crow + b) = 0u;
+    } else {
+      encode_store<G, FMT, RHO, NV>(v, inv, crow);
+    }
+  }
 }
 
 template <int R, int G, int FMT, int NV>
 __device__ __forceinline__ void quantize_tile_block(const typename Slot<R>::T (&v)[NV], int off, uint8_t* crow0,
-                                                    int64_t pitch, uint8_t* sfp, int nvalid, bool store_sf) {
+                                                    int64_t pitch, uint8_t* sfp, int nvalid, bool live, bool store_sf,
+                                                    bool zero) {
   uint32_t am[4];
-  block_amax<NV>(v, am);
-  quantize_row<0, G, FMT, NV>(v, am[0], off, crow0, sfp, nvalid > 0, store_sf);
-  if constexpr (R >= 2) quantize_row<1, G, FMT, NV>(v, am[1], off, crow0 + pitch, sfp, nvalid > 1, store_sf);
+  block_amax<NV>(v, am);   // every lane of the warp (full-warp shuffle)
+  quantize_row<0, G, FMT, NV>(v, am[0], off, crow0, sfp, live && nvalid > 0, store_sf, zero);
+  if constexpr (R >= 2) quantize_row<1, G, FMT, NV>(v, am[1], off, crow0 + pitch, sfp, live && nvalid > 1, store_sf, zero);
   if constexpr (R >= 4) {
-    quantize_row<2, G, FMT, NV>(v, am[2], off, crow0 + 2 * pitch, sfp, nvalid > 2, store_sf);
-    quantize_row<3, G, FMT, NV>(v, am[3], off, crow0 + 3 * pitch, sfp, nvalid > 3, store_sf);
+    quantize_row<2, G, FMT, NV>(v, am[2], off, crow0 + 2 * pitch, sfp, live && nvalid > 2, store_sf, zero);
+    quantize_row<3, G, FMT, NV>(v, am[3], off, crow0 + 3 * pitch, sfp, live && nvalid > 3, store_sf, zero);
   }
 }
 
 // Per-tile context of a consumer warp (everything seg_chunks needs besides the plan).
 template <int R> struct ChunkCtx {
   const uint8_t* st;        // stage: 256-channel boxes of row-interleaved slots
-  const uint32_t* gidx;     // gather table (byte offsets of slots, two per word) or null
+  const uint8_t* smem0;     // shared-memory base (the stage's offset from it is made warp-uniform)
+  const uint32_t* gidx;     // gather table: tab == 3: one u32 slot byte offset per reordered position;
+                            // tab == 1, 2: u16 offsets, two per word [block][16 words]; 0: none (L1 perm)
   const uint16_t* gamma_r;  // RMSNorm weight in reordered order (NORM only)
   int r0;                   // first row of the tile
   int nvalid;               // rows of the tile inside the matrix
   int group_warps, lane, dbg;
-  bool use_tab;
+  int tab;
 };
 
 // The chunks of segment G owned by this warp (local chunk c_first, c_first +
@@ -345,40 +375,54 @@ __device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& c
   const int kp = a.geom.kp[G], nb = (unsigned)kp >> 5, nch = (unsigned)(nb + 15) >> 4;
   if (c_first >= nch) return;
   const int n = a.geom.n[G], segoff = a.geom.off[G], sco = a.geom.sc_off[G];
-  const int64_t pitch = a.geom.pitch[G];
+  const uint32_t pitch = (uint32_t)a.geom.pitch[G];   // < 2^32 (K <= 65536)
   const int h = cx.lane & 1;                       // which half of the block
   constexpr int hb = G == 0 ? 8 : (G == 1 ? 12 : 16);   // code bytes per half block
   const unsigned r0 = (unsigned)cx.r0;
-  uint8_t* const crow_base = a.codes[G] + (int64_t)r0 * pitch + h * hb;
+  // the stage base through a warp reduction: a uniform register, so every gather load
+  // is one LDS [R + UR] with no per-slot address add
+  const uint32_t st_off = __reduce_max_sync(0xffffffffu, (uint32_t)(cx.st - cx.smem0));
+  const uint8_t* const st_u = cx.smem0 + st_off;
+  uint8_t* const crow_base = a.codes[G] + (uint64_t)r0 * pitch + h * hb;
   uint8_t* const sf_base = a.sf[G] + (size_t)((r0 >> 7) * ((unsigned)kp >> 7)) * 512 + (r0 & 31) * 16 + ((r0 >> 5) & 3) * 4;
+  // The chunk loop is warp-uniform and every lane runs the whole block path (the
+  // block amax combines the lane pair with a full-warp shuffle): lanes past the
+  // segment's last block compute on a valid block and store nothing; padding blocks
+  // (past n) gather block 0 and store zero codes and zero scale bytes.
   for (int c = c_first; c < nch; c += cx.group_warps) {
-    const int kb = c * 16 + (cx.lane >> 1);
-    if (kb >= nb) continue;                        // pair-uniform
+    const int kb_raw = c * 16 + (cx.lane >> 1);
+    const bool live = kb_raw < nb;                 // pair-uniform
+    const int kb = live ? kb_raw : nb - 1;
+    const bool pad = kb * 32 >= n || (cx.dbg & 8);
+    const int kbg = pad ? 0 : kb;                  // block whose channels are gathered
     uint8_t* crow0 = crow_base + (unsigned)kb * (2 * hb);
     uint8_t* sfp = sf_base + ((unsigned)kb >> 2) * 512 + (kb & 3);
-    if (kb * 32 >= n || (cx.dbg & 8)) {            // padding block: zero codes and zero scale bytes
-      if (cx.dbg & 16) continue;                   // timing experiment: no stores at all
-#pragma unroll
-      for (int rho = 0; rho < R; ++rho) {
-        if (h == 0) sfp[16 * rho] = 0;
-        if (rho < cx.nvalid)
-          for (int b = 0; b < hb; b += 4) *reinterpret_cast<uint32_t*>(crow0 + rho * pitch + b) = 0u;
-      }
-      continue;
-    }
+    if (MM_RQ_EXPERIMENTS && (cx.dbg & 16)) continue;   // timing experiment: no stores at all
     ST v[16];
-    if (cx.use_tab) {
-      const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + 16 * ((segoff >> 5) + kb) + 8 * h);
-      const uint4 p0 = gp[0], p1 = gp[1];
+    if (cx.tab == 3) {   // u32 offsets: 4 x 128-bit table loads, slot address = stage base + offset
+      const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + segoff + 32 * kbg + 16 * h);
+      const int rot = (cx.lane >> 1) & 3;          // the table build's per-lane rotation
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const uint4 e = gp[(q4 + rot) & 3];
+        v[4 * q4 + 0] = *reinterpret_cast<const ST*>(st_u + e.x);
+        v[4 * q4 + 1] = *reinterpret_cast<const ST*>(st_u + e.y);
+        v[4 * q4 + 2] = *reinterpret_cast<const ST*>(st_u + e.z);
+        v[4 * q4 + 3] = *reinterpret_cast<const ST*>(st_u + e.w);
+      }
+    } else if (cx.tab) {
+      const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + 16 * ((segoff >> 5) + kbg) + 8 * h);
+      const int rot = (cx.lane >> 2) & 1;          // the table build's per-lane swap
+      const uint4 p0 = gp[rot], p1 = gp[rot ^ 1];
       const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        v[2 * q + 0] = *reinterpret_cast<const ST*>(cx.st + (pr[q] & 0xFFFFu));
-        v[2 * q + 1] = *reinterpret_cast<const ST*>(cx.st + (pr[q] >> 16));
+        v[2 * q + 0] = *reinterpret_cast<const ST*>(st_u + (pr[q] & 0xFFFFu));
+        v[2 * q + 1] = *reinterpret_cast<const ST*>(st_u + (pr[q] >> 16));
       }
     } else {
       const ST* slots = reinterpret_cast<const ST*>(cx.st);
-      const int4* pp = reinterpret_cast<const int4*>(a.perm + segoff + 32 * kb + 16 * h);
+      const int4* pp = reinterpret_cast<const int4*>(a.perm + segoff + 32 * kbg + 16 * h);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int4 pv = __ldg(pp + q);
@@ -389,13 +433,13 @@ __device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& c
       }
     }
     if constexpr (NORM) {
-      const uint4* gp4 = reinterpret_cast<const uint4*>(cx.gamma_r + segoff + 32 * kb + 16 * h);
+      const uint4* gp4 = reinterpret_cast<const uint4*>(cx.gamma_r + segoff + 32 * kbg + 16 * h);
       const uint4 ga = gp4[0], gb = gp4[1];
       const uint32_t gw8[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
 #pragma unroll
       for (int i = 0; i < 16; ++i) norm_slot<R>(v[i], (gw8[i >> 1] >> (16 * (i & 1))) & 0xFFFFu, rn);
     }
-    quantize_tile_block<R, G, FMT, 16>(v, sco, crow0, pitch, sfp, cx.nvalid, h == 0);
+    quantize_tile_block<R, G, FMT, 16>(v, sco, crow0, pitch, sfp, cx.nvalid, live, live && h == 0, pad);
   }
 }
 
@@ -408,7 +452,8 @@ struct RqDev {
   int64_t n_tiles;      // tiles of R rows covering roundup(rows, 128)
   int nbox;             // TMA boxes of 256 channels per row
   int stages, groups, group_warps;
-  int perm_smem;        // 1: perm copied by bulk copy + gather table, 2: gather table built from global, 0: L1
+  int perm_smem;        // gather table: 3 = perm bulk-copied and turned IN PLACE into u32 slot offsets;
+                        // 1 = perm bulk-copied + u16 table; 2 = u16 table built from global; 0 = none (L1)
   int box3d;            // 1: one 3-D TMA per tile ({256, R, nbox} box), 0: nbox 2-D boxes
   int dbg;              // timing experiments only (env MM_RQ_DEBUG): 1 = skip gather/quantize, 2 = skip transpose too
 };
@@ -447,10 +492,11 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   const int stage_bytes = d.nbox * 512 * R;
   // [ring of stages][perm copy: K x int32][gather table: K x u16][barriers]
   const int K = a.K;
-  const size_t perm_copy = d.perm_smem == 1 ? (size_t)K * 4 : 0;
-  const size_t tab_bytes = d.perm_smem ? perm_copy + ((size_t)K * 2 + 15) / 16 * 16 : 0;
+  const size_t perm_copy = (d.perm_smem == 1 || d.perm_smem == 3) ? (size_t)K * 4 : 0;
+  const size_t tab_bytes = perm_copy + ((d.perm_smem == 1 || d.perm_smem == 2) ? ((size_t)K * 2 + 15) / 16 * 16 : 0);
   const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
-  uint32_t* gidx = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + perm_copy);   // K/2 words
+  uint32_t* gidx = d.perm_smem == 3 ? reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes)   // K words
+                                    : reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + perm_copy);  // K/2
   // optional RMSNorm region: gamma in reordered order (K x u16) + reduction scratch
   constexpr bool norm = NORM;   // RMSNorm fused ahead of the quantization (a.gamma != nullptr)
   const size_t norm_bytes = norm ? ((size_t)K * 2 + 255) / 256 * 256 + 4096 : 0;
@@ -460,7 +506,10 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)d.stages * stage_bytes + tab_bytes + norm_bytes);
   uint64_t* empty = full + d.stages;
   uint64_t* permbar = empty + d.stages;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index through a warp reduction: the compiler then knows it is warp-uniform, so
+  // the role / group / ring-slot values derived from it live in uniform registers and
+  // the gather's shared loads take the stage base as a uniform operand ([R + UR]).
+  const int warp = (int)__reduce_max_sync(0xffffffffu, threadIdx.x / 32), lane = threadIdx.x % 32;
   const uint64_t t_start = ptx::globaltimer_ns();
   if (threadIdx.x == 0 && (MM_RQ_EXPERIMENTS && (d.dbg & 32))) g_rq_trace[blockIdx.x][0] = t_start;
   if (threadIdx.x == 0) {
@@ -471,7 +520,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     ptx::mbar_init(ptx::smem_u32(permbar), 1);
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tmx);
-    if (d.perm_smem == 1) {  // the permutation arrives asynchronously, alongside the first tiles
+    if (d.perm_smem == 1 || d.perm_smem == 3) {  // the permutation arrives asynchronously, alongside the first tiles
       ptx::mbar_arrive_expect_tx(ptx::smem_u32(permbar), (uint32_t)K * 4);
       ptx::bulk_load(ptx::smem_u32(perm_s), a.perm, (uint32_t)K * 4, ptx::smem_u32(permbar));
     }
@@ -517,14 +566,44 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   // Gather table: u16 slot byte offsets, two per word, [block][16 words]: the lane
   // holding half h of block b reads words 16 b + 8 h .. + 7 with two 128-bit loads
   // (the warp reads 1 KB contiguously: conflict free).
-  const bool use_tab = d.perm_smem != 0;
-  if (use_tab) {
-    if (d.perm_smem == 1) ptx::mbar_wait(ptx::smem_u32(permbar), 0, 13, 0, 0);
+  const int tab = d.perm_smem;
+  if (tab) {
+    if (tab == 1 || tab == 3) ptx::mbar_wait(ptx::smem_u32(permbar), 0, 13, 0, 0);
     const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
-    for (int t = ct; t < K / 2; t += cn) {
-      const uint2 pr = d.perm_smem == 1 ? *reinterpret_cast<const uint2*>(perm_s + 2 * t)
-                                        : __ldg(reinterpret_cast<const uint2*>(a.perm + 2 * t));
-      gidx[t] = (pr.x * (uint32_t)sizeof(ST)) | ((pr.y * (uint32_t)sizeof(ST)) << 16);
+    // Table layouts are swizzled per lane so that the warp-wide 128-bit table loads of
+    // the gather are bank-conflict free: lane l of a chunk reads its vector q at
+    // "rotated" slot (q + rot(l)) of its own group (see seg_chunks).
+    const int off1 = a.geom.off[1], off2 = a.geom.off[2];
+    const uint32_t sz = (uint32_t)sizeof(ST);
+    if (tab == 3) {   // in place, one 16-position group per thread: perm[j] -> slot byte offset
+      for (int t = ct; t < K / 16; t += cn) {
+        const int j0 = 16 * t, segoff = j0 < off1 ? 0 : (j0 < off2 ? off1 : off2);
+        const int r = ((t - segoff / 16) >> 1) & 3;
+        uint4* g = reinterpret_cast<uint4*>(gidx) + 4 * t;
+        uint4 w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          w[q] = g[q];
+          w[q].x *= sz; w[q].y *= sz; w[q].z *= sz; w[q].w *= sz;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[(q + r) & 3] = w[q];
+      }
+    } else {          // u16 pairs, one 16-position group (8 words) per thread
+      for (int t = ct; t < K / 16; t += cn) {
+        const int j0 = 16 * t, segoff = j0 < off1 ? 0 : (j0 < off2 ? off1 : off2);
+        const int r = ((t - segoff / 16) >> 2) & 1;
+        uint4 pv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          pv[q] = tab == 1 ? reinterpret_cast<const uint4*>(perm_s)[4 * t + q]
+                           : __ldg(reinterpret_cast<const uint4*>(a.perm) + 4 * t + q);
+        uint4* g = reinterpret_cast<uint4*>(gidx) + 2 * t;
+        g[r] = make_uint4(pv[0].x * sz | (pv[0].y * sz) << 16, pv[0].z * sz | (pv[0].w * sz) << 16,
+                          pv[1].x * sz | (pv[1].y * sz) << 16, pv[1].z * sz | (pv[1].w * sz) << 16);
+        g[r ^ 1] = make_uint4(pv[2].x * sz | (pv[2].y * sz) << 16, pv[2].z * sz | (pv[2].w * sz) << 16,
+                              pv[3].x * sz | (pv[3].y * sz) << 16, pv[3].z * sz | (pv[3].w * sz) << 16);
+      }
     }
     ptx::named_bar_sync(15, cn);
     if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && threadIdx.x == 32) g_rq_trace[blockIdx.x][1] = ptx::globaltimer_ns();
@@ -533,7 +612,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   if constexpr (NORM) {   // gamma in reordered channel order
     const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
     for (int j = ct; j < K; j += cn) {
-      const int pj = d.perm_smem == 1 ? perm_s[j] : __ldg(a.perm + j);
+      const int pj = d.perm_smem == 1 ? perm_s[j] : __ldg(a.perm + j);   // (tab 3: perm_s already rewritten)
       gamma_r[j] = __ldg(a.gamma + pj);
     }
     ptx::named_bar_sync(15, cn);
@@ -640,10 +719,12 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) rn[rho] = (float)nred[32 * 8 + grp * 4 + rho];
       }
-      const int64_t r0 = (blockIdx.x + i * gridDim.x) * (int64_t)R;
+      // (through a warp reduction: a uniform register, so the per-tile row bases of the
+      // code / scale stores stay uniform instead of being rematerialised per store)
+      const int64_t r0 = (int64_t)__reduce_max_sync(0xffffffffu, (unsigned)((blockIdx.x + i * gridDim.x) * R));
       const int64_t left = rows - r0;
       const int nvalid = left >= R ? R : (left > 0 ? (int)left : 0);
-      const ChunkCtx<R> cx{st, gidx, gamma_r, (int)r0, nvalid, group_warps, lane, dbg, use_tab};
+      const ChunkCtx<R> cx{st, smem, gidx, gamma_r, (int)r0, nvalid, group_warps, lane, dbg, tab};
       seg_chunks<R, NORM, 0, F_E2M1>(a, cx, cf0, rn);
       if (e3m2) seg_chunks<R, NORM, 1, F_E3M2>(a, cx, cf1, rn);
       else seg_chunks<R, NORM, 1, F_E2M3>(a, cx, cf1, rn);
@@ -681,13 +762,23 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   // Gather table in smem: with an asynchronous copy of the permutation when that still
   // leaves >= 3 stages (mode 1), else built straight from global memory (mode 2: large K,
   // where the one-time prologue is amortised over many tiles), else none (L1 reads).
+  // Gather table: u32 slot offsets made in place from the bulk-copied permutation
+  // (mode 3: no offset unpacking in the gather, opt-in) when that leaves >= 3 stages; else u16
+  // offsets two per word, from a bulk copy (mode 1, >= 3 stages) or built straight from
+  // global memory (mode 2, >= 2 stages: large K, one-time prologue amortised over many
+  // tiles); else none (L1 reads of the permutation).
+  const size_t norm_need = a.gamma ? ((size_t)a.K * 2 + 255) / 256 * 256 + 4096 : 0;
+  const size_t budget = kRqSmemBudget - norm_need;
   const size_t gtab = ((size_t)a.K * 2 + 15) / 16 * 16;
   const size_t tab_need = (size_t)a.K * 4 + gtab;
-  d.perm_smem = (kRqSmemBudget - tab_need) / stage_bytes >= 3 ? 1 : ((kRqSmemBudget - gtab) / stage_bytes >= 2 ? 2 : 0);
-  if ((size_t)a.K * 2 * R > 65536) d.perm_smem = 0;   // table holds u16 slot byte offsets
-  const size_t tab_bytes = d.perm_smem == 1 ? tab_need : (d.perm_smem == 2 ? gtab : 0);
-  const size_t norm_need = a.gamma ? ((size_t)a.K * 2 + 255) / 256 * 256 + 4096 : 0;
-  int stages = (int)((kRqSmemBudget - tab_bytes - norm_need) / stage_bytes);
+  // Mode 3 is opt-in (MM_RQ_TAB32=1): measured 3 % slower than mode 1 at M = 16384,
+  // K = 4096 (the two extra table loads per lane cost more than the offset unpacking).
+  static const int tab32 = [] { const char* e = getenv("MM_RQ_TAB32"); return e ? atoi(e) : 0; }();
+  if (tab32 && a.K % 4 == 0 && (budget - (size_t)a.K * 4) / stage_bytes >= 3) d.perm_smem = 3;
+  else d.perm_smem = (budget - tab_need) / stage_bytes >= 3 ? 1 : ((budget - gtab) / stage_bytes >= 2 ? 2 : 0);
+  if (d.perm_smem != 3 && (size_t)a.K * 2 * R > 65536) d.perm_smem = 0;   // u16 table holds byte offsets
+  const size_t tab_bytes = d.perm_smem == 3 ? (size_t)a.K * 4 : (d.perm_smem == 1 ? tab_need : (d.perm_smem == 2 ? gtab : 0));
+  int stages = (int)((budget - tab_bytes) / stage_bytes);
   if (stages > 32) stages = 32;
   { const char* e = getenv("MM_RQ_STAGES"); if (e && atoi(e) >= 2 && atoi(e) < stages) stages = atoi(e); }
   if (stages < 2) return cudaErrorInvalidConfiguration;
