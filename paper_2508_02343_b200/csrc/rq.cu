@@ -639,7 +639,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     // registers, so the norm needs no second pass over the stage.)
     double nhi[4] = {0, 0, 0, 0}, nlo[4] = {0, 0, 0, 0};
     if constexpr (R > 1) {
-      for (int b = gw; b < nbox && dbg < 2; b += group_warps) {
+      for (int b = gw; b < nbox && !(dbg & 2); b += group_warps) {
         uint8_t* box = st + b * 512 * R;
         uint4 w[R];
 #pragma unroll
@@ -660,11 +660,17 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
         const uint32_t* u0 = reinterpret_cast<const uint32_t*>(&w[0]);
         const uint32_t* u1 = reinterpret_cast<const uint32_t*>(&w[1]);
         if constexpr (R == 2) {
+          // lane l writes 16-byte chunks 2l and 2l+1; lanes 4..7 of every 8 write their odd
+          // chunk first, so the 8 chunks of each store instruction fill 8 different bank
+          // groups (4 wavefronts per 512 B instead of 8)
           uint4* o = reinterpret_cast<uint4*>(box + lane * 32);
-          o[0] = make_uint4(__byte_perm(u0[0], u1[0], 0x5410), __byte_perm(u0[0], u1[0], 0x7632),
-                            __byte_perm(u0[1], u1[1], 0x5410), __byte_perm(u0[1], u1[1], 0x7632));
-          o[1] = make_uint4(__byte_perm(u0[2], u1[2], 0x5410), __byte_perm(u0[2], u1[2], 0x7632),
-                            __byte_perm(u0[3], u1[3], 0x5410), __byte_perm(u0[3], u1[3], 0x7632));
+          const uint4 c0 = make_uint4(__byte_perm(u0[0], u1[0], 0x5410), __byte_perm(u0[0], u1[0], 0x7632),
+                                      __byte_perm(u0[1], u1[1], 0x5410), __byte_perm(u0[1], u1[1], 0x7632));
+          const uint4 c1 = make_uint4(__byte_perm(u0[2], u1[2], 0x5410), __byte_perm(u0[2], u1[2], 0x7632),
+                                      __byte_perm(u0[3], u1[3], 0x5410), __byte_perm(u0[3], u1[3], 0x7632));
+          const bool f = (lane & 4) != 0;
+          o[f ? 1 : 0] = f ? c1 : c0;
+          o[f ? 0 : 1] = f ? c0 : c1;
         } else {
           const uint32_t* u2 = reinterpret_cast<const uint32_t*>(&w[2]);
           const uint32_t* u3 = reinterpret_cast<const uint32_t*>(&w[3]);
