@@ -397,7 +397,8 @@ def mm_comm_destroy(comm):
 
 
 def mm_mixed_gemm_bf16_nshard_allgather(a: MXTensor, w_shard: MXTensor, plan: Plan, n_total: int, comm,
-                                        out: torch.Tensor | None = None, stage: torch.Tensor | None = None):
+                                        out: torch.Tensor | None = None, stage: torch.Tensor | None = None,
+                                        stream=None):
     dev = plan.d_perm.device
     if out is None:
         out = torch.empty(a.rows, n_total, dtype=torch.bfloat16, device=dev)
@@ -406,7 +407,7 @@ def mm_mixed_gemm_bf16_nshard_allgather(a: MXTensor, w_shard: MXTensor, plan: Pl
     _check(lib().mm_mixed_gemm_bf16_nshard_allgather(ctypes.byref(a.c), ctypes.byref(w_shard.c),
                                                      ctypes.byref(plan.c), n_total, _ptr(out), out.stride(0),
                                                      _ptr(stage), stage.numel() * stage.element_size(), comm,
-                                                     _stream()))
+                                                     _stream(stream)))
     return out
 
 

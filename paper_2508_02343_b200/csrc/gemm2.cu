@@ -78,14 +78,15 @@ struct Gemm2Dev {
   int* ws_flag;                   // [npairs][8 epilogue warps]: 1 = that warp's 32 partial rows are
                                   // published; the one reader warp resets it to 0 after consuming
   int ndst;  // output maps used (1, or the peer window's world size)
+  int raster;  // pair-row blocks per raster group (8; MM_GEMM_RASTER for tuning)
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
 };
 
 // Tile raster: groups of up to 8 pair-row blocks (2048 rows of A) sweep all of N
 // before moving on, so a wave of tiles reuses the same A rows from L2 (for large M
 // the whole A does not fit in L2, W of one layer does).
-__device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& mb2, int& nb) {
-  const int G = num_m2 < 8 ? num_m2 : 8;
+__device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int raster, int& mb2, int& nb) {
+  const int G = num_m2 < raster ? num_m2 : raster;
   const int per_group = G * num_n;
   const int grp = t / per_group, r = t - grp * per_group;
   const int rows = min(G, num_m2 - grp * G);
@@ -215,7 +216,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         int t, s0, s1;
         work_item(p, pair, npairs, S, it, t, s0, s1);
         int mb2, nb;
-        tile_coords(t, num_m2, p.num_n, mb2, nb);
+        tile_coords(t, num_m2, p.num_n, p.raster, mb2, nb);
         const int m0 = mb2 * 256 + 128 * (int)rank;      // this CTA's A rows
         const int n0 = nb * 256 + 128 * (int)rank;       // this CTA's W rows (its half of N)
         const int mgrp = mb2 * 2 + (int)rank;           // 128-row scale group of A
@@ -367,7 +368,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       int t, s0, s1;
       work_item(p, pair, npairs, S, it, t, s0, s1);
       int mb2, nb;
-      tile_coords(t, num_m2, p.num_n, mb2, nb);
+      tile_coords(t, num_m2, p.num_n, p.raster, mb2, nb);
       // stream-K roles of this item: leave a partial (head of a tile) / add one (tail)
       const bool to_ws = s1 < S, from_ws = s0 > 0;
       const int wrow = 128 * (int)rank + q * 32 + lane;   // row inside the 256-row pair tile
@@ -607,6 +608,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.ldy = a.ldy;
   p.ndst = ndst;
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
+  { const char* r = getenv("MM_GEMM_RASTER"); p.raster = (r && atoi(r) > 0) ? atoi(r) : 8; }
   if (p.num_tiles == 0) return cudaSuccess;
   const int grid = pair_grid(a, cfg);
   const int npairs = grid / 2;
