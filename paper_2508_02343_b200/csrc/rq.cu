@@ -674,11 +674,21 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
         } else {
           const uint32_t* u2 = reinterpret_cast<const uint32_t*>(&w[2]);
           const uint32_t* u3 = reinterpret_cast<const uint32_t*>(&w[3]);
+          // lane l writes its 4 chunks in the order k = (j + l / 2) % 4: the 8 lanes of
+          // each 128-byte bank window then hit 8 different bank groups (4 wavefronts per
+          // 512 B store instruction instead of 16)
           uint4* o = reinterpret_cast<uint4*>(box + lane * 64);
+          uint4 c[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            o[k] = make_uint4(__byte_perm(u0[k], u1[k], 0x5410), __byte_perm(u2[k], u3[k], 0x5410),
+            c[k] = make_uint4(__byte_perm(u0[k], u1[k], 0x5410), __byte_perm(u2[k], u3[k], 0x5410),
                               __byte_perm(u0[k], u1[k], 0x7632), __byte_perm(u2[k], u3[k], 0x7632));
+          const int rot = (lane >> 1) & 3;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int k = (j + rot) & 3;
+            o[k] = k == 0 ? c[0] : (k == 1 ? c[1] : (k == 2 ? c[2] : c[3]));
+          }
         }
       }
       ptx::named_bar_sync(1 + grp, gthreads);
