@@ -79,6 +79,7 @@ struct Gemm2Dev {
                                   // published; the one reader warp resets it to 0 after consuming
   int ndst;  // output maps used (1, or the peer window's world size)
   int raster;  // pair-row blocks per raster group (8; MM_GEMM_RASTER for tuning)
+  int helpers; // 1: warps 0-3 drain half of the LAST tile's accumulator (data-parallel schedule)
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
 };
 
@@ -136,6 +137,33 @@ __device__ __forceinline__ void seg_stage(const Gemm2Dev& p, int j, int& kcoord,
   }
 }
 
+// Drain of accumulator columns [32 c_lo, 32 c_hi) of this CTA's 128 x 256 tile slab by
+// one warp (TMEM lane quadrant q): tcgen05.ld -> BF16 RNE -> 64B-swizzled staging
+// (one private 2 KB buffer per chunk) -> TMA store of each 32 x 32 box.
+template <int NP>
+__device__ __forceinline__ void drain_chunks(const YMaps<NP>& tys, int ndst, uint32_t trow, uint8_t* stg, int c_lo,
+                                             int c_hi, int n0, int row0, int lane) {
+  for (int c = c_lo; c < c_hi; ++c) {
+    uint32_t r[32];
+    ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
+    ptx::tc_wait_ld();
+    uint32_t w[16];
+#pragma unroll
+    for (int v = 0; v < 16; ++v) w[v] = ptx::pack_bf16x2(__uint_as_float(r[2 * v]), __uint_as_float(r[2 * v + 1]));
+    uint8_t* buf = stg + (c - c_lo) * 2048;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<uint4*>(buf + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) =
+          make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      for (int dst = 0; dst < (NP == 1 ? 1 : ndst); ++dst) ptx::tma_store_2d(&tys.m[dst], ptx::smem_u32(buf), n0 + 32 * c, row0);
+      ptx::bulk_commit_group();
+    }
+  }
+}
+
 template <int STAGES, int NP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
@@ -159,7 +187,8 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   uint64_t* tempty = tfull + 2;           // [2] accumulator fully drained (even CTA)
   uint64_t* tovl = tempty + 2;            // [2] overlap columns drained (even CTA)
   uint64_t* pbar = tovl + 2;              // [4] stream-K: a warp's partial rows landed in smem
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + 4);
+  uint64_t* hgo = pbar + 4;               // [1] helpers: the 4 epilogue warps reached the last tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hgo + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();    // 0 = MMA leader
@@ -186,6 +215,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(ptx::smem_u32(&pbar[i]), 1);
     }
+    ptx::mbar_init(ptx::smem_u32(hgo), 4);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), 512);
@@ -420,6 +450,19 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       const uint32_t acc_col = acc ? ACC1_COL : 0;
       uint32_t rn[32];   // chunk 1 of the drain order, loaded together with chunk 0
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc_col;
+      if (p.helpers && it == n_items - 1 && !(p.dbg & 4)) {
+        // last tile: warps 0-3 drain chunks 4-7 (drain_chunks below); these warps drain
+        // 0-3 into private staging buffers in the (now idle) operand ring.  The helpers
+        // are released through their own barrier, not tfull: a phase-parity wait on tfull
+        // from a warp that did not follow every earlier phase could alias an older one.
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(hgo));
+        if (lane == 0) ptx::bulk_wait_group_read<0>();   // this warp's earlier stores have read `stg`
+        __syncwarp();
+        drain_chunks<NP>(tys, p.ndst, trow, sA + (4 + q) * 8192, 0, 4, n0, row0, lane);
+        continue;
+      }
 #pragma unroll 1
       for (int i = 0; i < 8; ++i) {
         // acc0: its overlap (columns 208..255) lives in chunks 6, 7 -> drain those first;
@@ -507,6 +550,32 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       else ptx::bulk_wait_group<0>();   // peer stores fully performed before the CTA retires
     }
     if (trace && q == 0) g_trace[blockIdx.x][12] = ptx::globaltimer_ns();
+  }
+
+  if (warp < 4 && p.helpers && n_items > 0 && !(p.dbg & 4)) {
+    // ==================== helpers: drain of the last tile ====================
+    // The producer, MMA and allocator warps are idle once the last tile is issued; they
+    // drain columns 128..255 of its accumulator (their TMEM lane quadrant = warp % 4)
+    // while the epilogue warps drain columns 0..127, halving the exposed final drain.
+    __syncwarp();
+    const int it = n_items - 1;
+    int t, s0, s1;
+    work_item(p, pair, npairs, S, it, t, s0, s1);
+    int mb2, nb;
+    tile_coords(t, num_m2, p.num_n, p.raster, mb2, nb);
+    const int acc = it & 1;
+    // single phase: the epilogue warps saw tfull.  A suspended wait: warps 1 (odd CTA)
+    // and 2 have no role and would otherwise spin for the whole kernel, stealing issue
+    // slots from the epilogue.
+    ptx::mbar_wait_sleep(ptx::smem_u32(hgo), 0, 26, it, t);
+    ptx::tc_fence_after();
+    const int q = warp & 3;
+    const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + (acc ? ACC1_COL : 0);
+    drain_chunks<NP>(tys, p.ndst, trow, sA + q * 8192, 4, 8, nb * 256, mb2 * 256 + 128 * (int)rank + q * 32, lane);
+    if (lane == 0) {
+      if constexpr (NP == 1) ptx::bulk_wait_group_read<0>();
+      else ptx::bulk_wait_group<0>();
+    }
   }
 
   ptx::tc_fence_before();
@@ -613,6 +682,14 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   const int grid = pair_grid(a, cfg);
   const int npairs = grid / 2;
   p.stream_k = use_stream_k(a, cfg) ? 1 : 0;
+  // Helper drain of the last tile: for few tiles per pair (<= 4), where the exposed final
+  // drain is a visible share of the kernel (q_proj: 27 -> 25 us); measured ~1 % slower
+  // with ~14 tiles per pair (70B down_proj), so off there.  MM_GEMM_HELPERS=0/1 forces it.
+  {
+    const char* h = getenv("MM_GEMM_HELPERS");
+    const bool want = h ? atoi(h) == 1 : p.num_tiles <= 4 * npairs;
+    p.helpers = (!p.stream_k && want) ? 1 : 0;
+  }
   if (p.stream_k) {   // caller workspace: [flags npairs x 8 ints, 256-B padded][partials]
     if (!a.ws || a.ws_bytes < pair_workspace_bytes(a, cfg)) {
       *err = "stream-K workspace missing or too small";
@@ -621,7 +698,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
     p.ws_flag = static_cast<int*>(a.ws);
     p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a.ws) + ws_align((size_t)npairs * 8 * sizeof(int)));
   }
-  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + epi_bytes<STAGES>() + (2 * STAGES + 10) * 8 + 16;
+  const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + epi_bytes<STAGES>() + (2 * STAGES + 11) * 8 + 16;
   auto kern = mixgemm2_kernel<STAGES, NP>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }

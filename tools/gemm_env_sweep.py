@@ -33,7 +33,8 @@ for arg in sys.argv[1:]:
             k, val = kv.split("=")
             saved[k] = os.environ.get(k)
             os.environ[k] = val
-        us = sc.time_loop(lambda i: mm.mm_mixed_gemm_bf16(aa[i], ws[i], plan, out=ys[i]), n, 40)
+        us = sc.time_loop(lambda i: mm.mm_mixed_gemm_bf16(aa[i], ws[i], plan, out=ys[i]), n, int(os.environ.get("REPS", "40")))
+        if os.environ.get("PAUSE"): torch.cuda.synchronize(); import time as _t; _t.sleep(float(os.environ["PAUSE"]))
         tf = 2.0 * M * N * K / (us * 1e-6) / 1e12
         res.append(f"[{v or 'default'}] {us:.2f}us {tf / pmix:.3f}")
         for k, old in saved.items():
