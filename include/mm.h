@@ -96,6 +96,9 @@ typedef struct {
   double t4, t6;        /* T(4), T(6) of Eq. 5 (0 for user plans)                 */
   int32_t c[3];         /* raw channel counts before rounding to 32 (calibration) */
   int32_t reserved2;
+  const uint32_t* d_layout; /* optional gather-slot layout (mm_plan_set_gather_layout); NULL =
+                               natural.  Changes where the RQ keeps values in shared memory only:
+                               results are identical with and without it (borrowed). */
 } mm_plan;
 
 /* One quantized operand (activation: rows = M; weight: rows = N). */
@@ -118,6 +121,22 @@ int64_t mm_calib_workspace_bytes(int64_t L, int32_t K);
 mm_status mm_plan_init(mm_plan* plan_out, int32_t K, const int32_t n[3], int32_t fmt6,
                        int32_t fmt8, int32_t rule, const int32_t* h_perm,
                        int32_t* d_perm_storage, mm_stream_t stream);
+
+/* Plan-time gather layout for the reorder-quantize (an implementation choice, not part
+ * of the method: DESIGN.md §6.1).  For the plan's permutation, a local search picks,
+ * inside every 32-channel line of the RQ's shared-memory rows, a parity-preserving
+ * permutation of its eight 4-channel chunks that lowers the bank conflicts of the
+ * gather x_r[j] = X[perm[j]].  d_layout_storage: caller device buffer of
+ * mm_gather_layout_words(K) u32 words; on success plan->d_layout points to it.  Reads the
+ * permutation back and SYNCHRONIZES stream (offline call).  Quantized outputs do not
+ * depend on it (the plan fingerprint is unchanged). */
+int64_t mm_gather_layout_words(int32_t K);
+mm_status mm_plan_set_gather_layout(mm_plan* plan, uint32_t* d_layout_storage, mm_stream_t stream);
+/* Host-only forms (diagnostics / tests): the layout for (K, n, permutation) into
+ * h_layout_out[K/32], and the gather's bank wavefronts for a layout (NULL = natural);
+ * -1 on invalid arguments. */
+mm_status mm_gather_layout_host(int32_t K, const int32_t n[3], const int32_t* h_perm, uint32_t* h_layout_out);
+int64_t mm_gather_wavefronts(int32_t K, const int32_t n[3], const int32_t* h_perm, const uint32_t* h_layout);
 
 /* Offline calibration (§3.1 Q1-Q3, Eq. 5-7, Eq. 17; §4.1).
  * d_x: BF16 [L, K] calibration activations (ld = ldx).  On the device: exact

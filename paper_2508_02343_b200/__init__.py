@@ -33,7 +33,8 @@ EXPORTS = [
     "mm_padded_cols", "mm_code_pitch_bytes", "mm_codes_bytes", "mm_sf_bytes",
     "mm_calib_workspace_bytes", "mm_plan_init", "mm_calibrate_thresholds",
     "mm_quantize_weight_offline", "mm_reorder_quantize_act", "mm_mixed_gemm_bf16", "mm_gemm_workspace_bytes",
-    "mm_peer_window_set_timeout", "mm_peer_window_error",
+    "mm_peer_window_set_timeout", "mm_peer_window_error", "mm_gather_layout_words", "mm_plan_set_gather_layout",
+    "mm_gather_layout_host", "mm_gather_wavefronts",
     "mm_reorder_act_bf16", "mm_set_gemm_config", "mm_launch_count", "mm_reset_launch_count",
     "mm_last_error", "mm_abi_version", "mm_nccl_unique_id_bytes", "mm_nccl_get_unique_id",
     "mm_comm_init", "mm_comm_destroy", "mm_mixed_gemm_bf16_nshard_allgather",
@@ -56,7 +57,7 @@ class CPlan(ctypes.Structure):
                 ("fmt8", ctypes.c_int32), ("rule", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("d_perm", ctypes.c_void_p), ("fingerprint", ctypes.c_uint64),
                 ("tensor_max", ctypes.c_double), ("t4", ctypes.c_double), ("t6", ctypes.c_double),
-                ("c", ctypes.c_int32 * 3), ("reserved2", ctypes.c_int32)]
+                ("c", ctypes.c_int32 * 3), ("reserved2", ctypes.c_int32), ("d_layout", ctypes.c_void_p)]
 
 
 class CDiag(ctypes.Structure):
@@ -99,6 +100,10 @@ def lib(build_if_missing: bool = False):
             "mm_reorder_quantize_act": (ctypes.c_int, [vp, i64, i64, P, X, vp]),
             "mm_mixed_gemm_bf16": (ctypes.c_int, [X, X, P, vp, i64, vp, ctypes.c_size_t, vp]),
             "mm_gemm_workspace_bytes": (i64, [P, i64, i64]),
+            "mm_gather_layout_words": (i64, [i32]),
+            "mm_plan_set_gather_layout": (ctypes.c_int, [P, vp, vp]),
+            "mm_gather_layout_host": (ctypes.c_int, [i32, ctypes.POINTER(i32), vp, vp]),
+            "mm_gather_wavefronts": (i64, [i32, ctypes.POINTER(i32), vp, vp]),
             "mm_reorder_act_bf16": (ctypes.c_int, [vp, i64, i64, P, vp, i64, vp]),
             "mm_set_gemm_config": (ctypes.c_int, [i32, i32, i32]),
             "mm_launch_count": (i64, []),
@@ -152,9 +157,21 @@ def _ptr(t: torch.Tensor):
 class Plan:
     """A channel plan (include/mm.h mm_plan) plus the device permutation it borrows."""
 
-    def __init__(self, c: CPlan, d_perm: torch.Tensor):
+    def __init__(self, c: CPlan, d_perm: torch.Tensor, layout: bool | None = None):
         self.c = c
         self.d_perm = d_perm
+        self.d_layout = None
+        if layout is None:
+            layout = os.environ.get("MM_NO_GATHER_LAYOUT", "0") != "1"
+        if layout:
+            self.set_gather_layout()
+
+    def set_gather_layout(self, stream=None):
+        """Attach the plan-time gather layout (mm_plan_set_gather_layout; offline, synchronizes)."""
+        words = int(lib().mm_gather_layout_words(self.c.K))
+        buf = torch.empty(max(words, 4), dtype=torch.int32, device=self.d_perm.device)
+        _check(lib().mm_plan_set_gather_layout(ctypes.byref(self.c), _ptr(buf), _stream(stream)))
+        self.d_layout = buf
 
     @property
     def K(self):

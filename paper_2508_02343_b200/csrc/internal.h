@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <cstdint>
+#include <vector>
 #include <cstdlib>
 #include <utility>
 
@@ -35,9 +36,14 @@ struct RqArgs {
   SegGeom geom;
   uint8_t* codes[3];
   uint8_t* sf[3];
+  const uint32_t* layout; // gather-slot layout (one u32 per 32-channel line) or nullptr (layout.cpp)
   const uint16_t* gamma;  // BF16 [K] RMSNorm weight, or nullptr (no norm; F2 fusion)
   double eps;             // RMSNorm epsilon (> 0) when gamma != nullptr
 };
+
+// Plan-time gather layout (layout.cpp).
+std::vector<uint32_t> gather_layout(int K, const int n[3], const int32_t* perm);
+long long gather_wavefronts(int K, const int n[3], const int32_t* perm, const uint32_t* layout);
 
 // Fused reorder-and-quantize (rq.cu).
 cudaError_t launch_reorder_quantize(const RqArgs& a, cudaStream_t s, int64_t* launches);

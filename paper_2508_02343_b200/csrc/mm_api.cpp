@@ -181,6 +181,7 @@ mm_status run_rq(const void* d_x, int64_t rows, int64_t ldx, const mm_plan* plan
   a.ldx = ldx;
   a.K = plan->K;
   a.perm = plan->d_perm;
+  a.layout = plan->d_layout;
   a.geom = geom_of(plan);
   a.gamma = static_cast<const uint16_t*>(d_gamma);
   a.eps = eps;
@@ -243,7 +244,7 @@ using namespace mmx;
 
 extern "C" {
 
-int32_t mm_abi_version(void) { return 2; }   // 2: caller GEMM workspace, N-shard stage bytes, peer timeout
+int32_t mm_abi_version(void) { return 3; }   // 2: caller GEMM workspace, N-shard stage bytes, peer timeout; 3: plan gather layout
 const char* mm_last_error(void) { return g_err.c_str(); }
 int64_t mm_launch_count(void) { return g_launches; }
 void mm_reset_launch_count(void) { g_launches = 0; }
@@ -303,6 +304,52 @@ mm_status mm_plan_init(mm_plan* out, int32_t K, const int32_t n[3], int32_t fmt6
   out->rule = rule;
   out->d_perm = d_perm_storage;
   out->fingerprint = fingerprint(K, n, fmt6, fmt8, rule, h_perm);
+  return MM_OK;
+}
+
+int64_t mm_gather_layout_words(int32_t K) { return (K > 0 && K % 32 == 0) ? K / 32 : -1; }
+
+static bool layout_args_ok(int32_t K, const int32_t n[3], const int32_t* h_perm) {
+  if (!n || !h_perm || K <= 0 || K % 32 != 0 || K > 65536) return false;
+  int64_t sum = 0;
+  for (int g = 0; g < 3; ++g) {
+    if (n[g] < 0 || n[g] % 32 != 0) return false;
+    sum += n[g];
+  }
+  if (sum != K) return false;
+  for (int32_t j = 0; j < K; ++j)
+    if (h_perm[j] < 0 || h_perm[j] >= K) return false;
+  return true;
+}
+
+mm_status mm_gather_layout_host(int32_t K, const int32_t n[3], const int32_t* h_perm, uint32_t* h_layout_out) {
+  if (!h_layout_out || !layout_args_ok(K, n, h_perm)) return fail(MM_ERR_INVALID_ARGUMENT, "bad K / n / permutation");
+  const std::vector<uint32_t> lay = gather_layout(K, n, h_perm);
+  std::memcpy(h_layout_out, lay.data(), lay.size() * 4);
+  return MM_OK;
+}
+
+int64_t mm_gather_wavefronts(int32_t K, const int32_t n[3], const int32_t* h_perm, const uint32_t* h_layout) {
+  if (!layout_args_ok(K, n, h_perm)) return -1;
+  return gather_wavefronts(K, n, h_perm, h_layout);
+}
+
+mm_status mm_plan_set_gather_layout(mm_plan* plan, uint32_t* d_layout_storage, mm_stream_t stream) {
+  mm_status st = validate_plan(plan);
+  if (st != MM_OK) return st;
+  if (!d_layout_storage || !aligned(d_layout_storage, 16))
+    return fail(MM_ERR_ALIGNMENT, "layout storage must be non-NULL and 16-byte aligned");
+  const int K = plan->K;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<int32_t> perm(K);
+  cudaError_t e = cudaMemcpyAsync(perm.data(), plan->d_perm, (size_t)K * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "read the permutation");
+  const std::vector<uint32_t> lay = gather_layout(K, plan->n, perm.data());
+  e = cudaMemcpyAsync(d_layout_storage, lay.data(), lay.size() * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "upload the layout");
+  plan->d_layout = d_layout_storage;
   return MM_OK;
 }
 

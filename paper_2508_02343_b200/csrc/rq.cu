@@ -493,7 +493,11 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   // [ring of stages][perm copy: K x int32][gather table: K x u16][barriers]
   const int K = a.K;
   const size_t perm_copy = (d.perm_smem == 1 || d.perm_smem == 3) ? (size_t)K * 4 : 0;
-  const size_t tab_bytes = perm_copy + ((d.perm_smem == 1 || d.perm_smem == 2) ? ((size_t)K * 2 + 15) / 16 * 16 : 0);
+  // (+ the gather layout's per-line words for the transpose, R = 2 only)
+  const size_t tab_core = perm_copy + ((d.perm_smem == 1 || d.perm_smem == 2) ? ((size_t)K * 2 + 15) / 16 * 16 : 0);
+  const uint32_t* layout = R == 2 ? a.layout : nullptr;
+  const size_t tab_bytes = tab_core + (layout ? ((size_t)(K / 32) * 4 + 15) / 16 * 16 : 0);
+  uint32_t* lay_s = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + tab_core);
   const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
   uint32_t* gidx = d.perm_smem == 3 ? reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes)   // K words
                                     : reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + perm_copy);  // K/2
@@ -575,6 +579,13 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     // "rotated" slot (q + rot(l)) of its own group (see seg_chunks).
     const int off1 = a.geom.off[1], off2 = a.geom.off[2];
     const uint32_t sz = (uint32_t)sizeof(ST);
+    // slot of channel p: the layout moves 4-channel chunks inside each 32-channel line
+    auto slot = [layout](uint32_t p) -> uint32_t {
+      if (!layout) return p;
+      return (p & ~31u) | (((__ldg(layout + (p >> 5)) >> (4 * ((p >> 2) & 7))) & 7u) << 2) | (p & 3u);
+    };
+    if (layout)
+      for (int t = ct; t < K / 32; t += cn) lay_s[t] = __ldg(layout + t);
     if (tab == 3) {   // in place, one 16-position group per thread: perm[j] -> slot byte offset
       for (int t = ct; t < K / 16; t += cn) {
         const int j0 = 16 * t, segoff = j0 < off1 ? 0 : (j0 < off2 ? off1 : off2);
@@ -584,7 +595,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           w[q] = g[q];
-          w[q].x *= sz; w[q].y *= sz; w[q].z *= sz; w[q].w *= sz;
+          w[q].x = slot(w[q].x) * sz; w[q].y = slot(w[q].y) * sz; w[q].z = slot(w[q].z) * sz; w[q].w = slot(w[q].w) * sz;
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) g[(q + r) & 3] = w[q];
@@ -599,10 +610,15 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
           pv[q] = tab == 1 ? reinterpret_cast<const uint4*>(perm_s)[4 * t + q]
                            : __ldg(reinterpret_cast<const uint4*>(a.perm) + 4 * t + q);
         uint4* g = reinterpret_cast<uint4*>(gidx) + 2 * t;
-        g[r] = make_uint4(pv[0].x * sz | (pv[0].y * sz) << 16, pv[0].z * sz | (pv[0].w * sz) << 16,
-                          pv[1].x * sz | (pv[1].y * sz) << 16, pv[1].z * sz | (pv[1].w * sz) << 16);
-        g[r ^ 1] = make_uint4(pv[2].x * sz | (pv[2].y * sz) << 16, pv[2].z * sz | (pv[2].w * sz) << 16,
-                              pv[3].x * sz | (pv[3].y * sz) << 16, pv[3].z * sz | (pv[3].w * sz) << 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          pv[q].x = slot(pv[q].x) * sz; pv[q].y = slot(pv[q].y) * sz;
+          pv[q].z = slot(pv[q].z) * sz; pv[q].w = slot(pv[q].w) * sz;
+        }
+        g[r] = make_uint4(pv[0].x | pv[0].y << 16, pv[0].z | pv[0].w << 16, pv[1].x | pv[1].y << 16,
+                          pv[1].z | pv[1].w << 16);
+        g[r ^ 1] = make_uint4(pv[2].x | pv[2].y << 16, pv[2].z | pv[2].w << 16, pv[3].x | pv[3].y << 16,
+                              pv[3].z | pv[3].w << 16);
       }
     }
     ptx::named_bar_sync(15, cn);
@@ -663,14 +679,23 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
           // lane l writes 16-byte chunks 2l and 2l+1; lanes 4..7 of every 8 write their odd
           // chunk first, so the 8 chunks of each store instruction fill 8 different bank
           // groups (4 wavefronts per 512 B instead of 8)
-          uint4* o = reinterpret_cast<uint4*>(box + lane * 32);
           const uint4 c0 = make_uint4(__byte_perm(u0[0], u1[0], 0x5410), __byte_perm(u0[0], u1[0], 0x7632),
                                       __byte_perm(u0[1], u1[1], 0x5410), __byte_perm(u0[1], u1[1], 0x7632));
           const uint4 c1 = make_uint4(__byte_perm(u0[2], u1[2], 0x5410), __byte_perm(u0[2], u1[2], 0x7632),
                                       __byte_perm(u0[3], u1[3], 0x5410), __byte_perm(u0[3], u1[3], 0x7632));
           const bool f = (lane & 4) != 0;
-          o[f ? 1 : 0] = f ? c1 : c0;
-          o[f ? 0 : 1] = f ? c0 : c1;
+          // chunk positions inside this lane's 128-byte line: natural, or the plan's
+          // parity-preserving gather layout (an odd chunk stays odd: still 8 bank groups
+          // per store instruction)
+          int p0 = 2 * (lane & 3), p1 = p0 + 1;
+          if (layout) {
+            const uint32_t lw = lay_s[8 * b + (lane >> 2)];
+            p0 = (lw >> (4 * p0)) & 7;
+            p1 = (lw >> (4 * p1)) & 7;
+          }
+          uint4* line = reinterpret_cast<uint4*>(box + (lane >> 2) * 128);
+          line[f ? p1 : p0] = f ? c1 : c0;
+          line[f ? p0 : p1] = f ? c0 : c1;
         } else {
           const uint32_t* u2 = reinterpret_cast<const uint32_t*>(&w[2]);
           const uint32_t* u3 = reinterpret_cast<const uint32_t*>(&w[3]);
@@ -793,7 +818,11 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   if (tab32 && a.K % 4 == 0 && (budget - (size_t)a.K * 4) / stage_bytes >= 3) d.perm_smem = 3;
   else d.perm_smem = (budget - tab_need) / stage_bytes >= 3 ? 1 : ((budget - gtab) / stage_bytes >= 2 ? 2 : 0);
   if (d.perm_smem != 3 && (size_t)a.K * 2 * R > 65536) d.perm_smem = 0;   // u16 table holds byte offsets
-  const size_t tab_bytes = d.perm_smem == 3 ? (size_t)a.K * 4 : (d.perm_smem == 1 ? tab_need : (d.perm_smem == 2 ? gtab : 0));
+  size_t tab_bytes = d.perm_smem == 3 ? (size_t)a.K * 4 : (d.perm_smem == 1 ? tab_need : (d.perm_smem == 2 ? gtab : 0));
+  // gather layout (R = 2 with a table only): per-line words for the transpose
+  static const int no_layout = [] { const char* e = getenv("MM_RQ_NO_LAYOUT"); return e ? atoi(e) : 0; }();  // A/B
+  if (R != 2 || d.perm_smem == 0 || no_layout) d.a.layout = nullptr;
+  if (d.a.layout) tab_bytes += ((size_t)(a.K / 32) * 4 + 15) / 16 * 16;
   int stages = (int)((budget - tab_bytes) / stage_bytes);
   if (stages > 32) stages = 32;
   { const char* e = getenv("MM_RQ_STAGES"); if (e && atoi(e) >= 2 && atoi(e) < stages) stages = atoi(e); }

@@ -32,7 +32,7 @@ def test_header_matches_binding_list():
 def test_library_exports_every_symbol(L):
     for name in _header_symbols():
         assert hasattr(L, name), name
-    assert L.mm_abi_version() == 2
+    assert L.mm_abi_version() == 3
 
 
 def _plan(K, n, fmt6=mm.MM_E3M2, fmt8=mm.MM_E4M3):
@@ -132,3 +132,23 @@ def test_gemm_config_values(L):
         assert L.mm_set_gemm_config(bn, 0, 0) == 0
     assert L.mm_set_gemm_config(64, 0, 0) == 1
     assert L.mm_set_gemm_config(0, 0, 0) == 0
+
+
+def test_gather_layout_host(L):
+    """The plan-time gather layout (layout.cpp): per 32-channel line a
+    parity-preserving permutation of the eight 4-channel chunks, with fewer gather bank
+    wavefronts than the natural layout for a calibrated-like permutation."""
+    import numpy as np
+    K, n = 4096, (2240, 1184, 672)
+    perm = np.random.default_rng(3).permutation(K).astype(np.int32)
+    nn = (ctypes.c_int32 * 3)(*n)
+    lay = np.zeros(K // 32, dtype=np.uint32)
+    assert L.mm_gather_layout_host(K, nn, perm.ctypes.data, lay.ctypes.data) == 0
+    for w in lay:
+        pos = [(int(w) >> (4 * c)) & 15 for c in range(8)]
+        assert sorted(pos) == list(range(8))
+        assert all(pos[c] % 2 == c % 2 for c in range(8))
+    nat = L.mm_gather_wavefronts(K, nn, perm.ctypes.data, None)
+    opt = L.mm_gather_wavefronts(K, nn, perm.ctypes.data, lay.ctypes.data)
+    assert 0 < opt <= 0.85 * nat, (nat, opt)
+    assert L.mm_gather_layout_host(K + 1, nn, perm.ctypes.data, lay.ctypes.data) == 1

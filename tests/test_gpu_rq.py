@@ -178,3 +178,24 @@ def test_rmsnorm_rejects_bad_eps():
     g = torch.ones(256, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(mm.MMError):
         mm.mm_rmsnorm_reorder_quantize_act(x, g, 0.0, plan)
+
+
+@pytest.mark.parametrize("K,n", [(4096, (2240, 1184, 672)), (14336, (8512, 3840, 1984))])
+def test_gather_layout_does_not_change_results(K, n):
+    """The plan-time gather layout (mm_plan_set_gather_layout) only moves values inside
+    shared memory: codes and scales equal those of the natural layout, byte for byte,
+    and the oracle's."""
+    perm = gen_perm(K, 77)
+    x = gen_act(300, K, 1000, 2077)
+    p_nat = mm.mm_plan_init(K, n, perm)
+    p_nat.c.d_layout = None
+    p_nat.d_layout = None
+    p_lay = mm.mm_plan_init(K, n, perm)
+    assert p_lay.d_layout is not None and p_lay.c.d_layout
+    a0 = mm.mm_reorder_quantize_act(x.cuda(), p_nat)
+    a1 = mm.mm_reorder_quantize_act(x.cuda(), p_lay)
+    torch.cuda.synchronize()
+    for g in range(3):
+        if n[g]:
+            assert torch.equal(a0.codes2d(g), a1.codes2d(g)), g
+    _parity(x, p_lay)
