@@ -484,6 +484,31 @@ def run_gpu(args, rank, world, local):
                 "allgather_bytes": 2 * M * N,
                 "allgather_note": "torch.distributed all_gather_into_tensor (NCCL) of the same BF16 bytes, "
                                   "busbw = (G-1)/G x bytes / time"}
+            if mm.mc_supported():   # NVLS: each element written once via multimem.st, switch replicates
+                mwin = mm.McWindow.create(M, N)
+                try:
+                    def nvls_step(i):
+                        st_ = sets[i % n_sets]
+                        mm.mm_reorder_quantize_act(st_["x"], plan, out=st_["a"], stream=stream)
+                        mm.mm_mixed_gemm_bf16_nshard_nvls(st_["a"], st_["wq"], plan, N, mwin, barrier=True,
+                                                          stream=stream)
+                    for i in range(args.warmup):
+                        nvls_step(i)
+                    barrier(world)
+                    torch.cuda.synchronize()
+                    v_total, _ = timed_chunks(stream, args.steps, nvls_step, min(400.0, sleep_ms))
+                    barrier(world)
+                    v_ms = max_over_ranks(v_total, world) / args.steps
+                    extra_nshard["nvls_allgather"] = {
+                        "value": 2.0 * M * N * K / (v_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": v_ms,
+                        "what": "RQ + GEMM whose epilogue writes each element once through a multicast object "
+                                "(multimem.st over NVLink SHARP) + multimem.red flag barrier"}
+                finally:
+                    torch.cuda.synchronize()
+                    barrier(world)
+                    mwin.close()
+            else:
+                extra_nshard["nvls_allgather"] = "unavailable: this GPU cannot create multicast objects"
             if win is not None:   # the fused all-gather epilogue on the same ranks
                 barrier(world)
                 torch.cuda.synchronize()

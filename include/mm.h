@@ -311,6 +311,39 @@ mm_status mm_mixed_gemm_bf16_nshard_peerstore(const mm_mx_tensor* a, const mm_mx
                                               const mm_plan* plan, int64_t n_total, void* win,
                                               int32_t barrier, mm_stream_t stream);
 mm_status mm_peer_barrier(void* win, mm_stream_t stream);
+/* ---- fused all-gather over NVLS / NVLink SHARP (multicast) ----
+ * One multicast object spans every rank's buffer ([Y: BF16 M x ldy, padded to 256 B]
+ * [flags: 64 x u32], the peer-buffer layout); the CTA-pair GEMM epilogue writes each
+ * output element ONCE with multimem.st and the switch replicates it to all ranks
+ * (per-GPU egress M*Ns*2 bytes instead of (G-1)*M*Ns*2).  Setup is collective, in two
+ * halves separated by a barrier of the caller's process group:
+ *   1. mm_mc_window_create on every rank: rank 0 creates the object and writes its
+ *      shareable handle (mm_mc_handle_bytes() bytes: a fabric handle, else a POSIX fd
+ *      that the peers duplicate with pidfd_getfd) into h_handle; the caller broadcasts
+ *      those bytes and the other ranks pass them in; every rank adds its device.
+ *   2. (barrier) mm_mc_window_bind on every rank: allocates this rank's buffer with the
+ *      driver's virtual-memory API, binds it, maps the multicast and the local views and
+ *      zeroes the buffer; (barrier) before the first GEMM.
+ * mm_mc_window_local returns this rank's buffer (read Y there).  world <= 8; world 1 is
+ * allowed (a one-device multicast object, for testing).  mm_mc_supported() reports
+ * whether this device can create multicast objects (attribute + a one-time probe: GPUs
+ * not attached to an NVSwitch fabric reject cuMulticastCreate).  Barrier: every rank adds 1 to flag word 0 of all ranks through the
+ * multicast view (multimem.red.release.sys) and waits for its own copy to reach
+ * world * epoch; with a timeout (mm_mc_window_set_timeout, default off) a barrier that
+ * gives up writes 0xFFFF into flag word 63, reported by mm_mc_window_error.
+ * mm_mixed_gemm_bf16_nshard_nvls: as mm_mixed_gemm_bf16_nshard_peerstore. */
+int32_t mm_mc_supported(void);
+int32_t mm_mc_handle_bytes(void);
+mm_status mm_mc_window_create(int32_t rank, int32_t world, int64_t M, int64_t ldy, void* h_handle, void** win_out);
+mm_status mm_mc_window_bind(void* win);
+void* mm_mc_window_local(void* win);
+mm_status mm_mc_window_set_timeout(void* win, double seconds);
+mm_status mm_mc_window_error(void* win, int32_t* h_timed_out);   /* synchronous; 1 if a barrier gave up */
+mm_status mm_mc_window_close(void* win);
+mm_status mm_mc_barrier(void* win, mm_stream_t stream);
+mm_status mm_mixed_gemm_bf16_nshard_nvls(const mm_mx_tensor* a, const mm_mx_tensor* w_shard, const mm_plan* plan,
+                                         int64_t n_total, void* win, int32_t barrier, mm_stream_t stream);
+
 /* Barrier timeout of a window (default 0 = wait forever, like NCCL: a slow rank is
  * not an error).  With a timeout, a barrier whose peer never arrives gives up, and
  * records the missing rank in this rank's buffer instead of trapping (the CUDA

@@ -34,7 +34,9 @@ EXPORTS = [
     "mm_calib_workspace_bytes", "mm_plan_init", "mm_calibrate_thresholds",
     "mm_quantize_weight_offline", "mm_reorder_quantize_act", "mm_mixed_gemm_bf16", "mm_gemm_workspace_bytes",
     "mm_peer_window_set_timeout", "mm_peer_window_error", "mm_gather_layout_words", "mm_plan_set_gather_layout",
-    "mm_gather_layout_host", "mm_gather_wavefronts",
+    "mm_gather_layout_host", "mm_gather_wavefronts", "mm_mc_supported", "mm_mc_handle_bytes",
+    "mm_mc_window_create", "mm_mc_window_bind", "mm_mc_window_local", "mm_mc_window_set_timeout",
+    "mm_mc_window_error", "mm_mc_window_close", "mm_mc_barrier", "mm_mixed_gemm_bf16_nshard_nvls",
     "mm_reorder_act_bf16", "mm_set_gemm_config", "mm_launch_count", "mm_reset_launch_count",
     "mm_last_error", "mm_abi_version", "mm_nccl_unique_id_bytes", "mm_nccl_get_unique_id",
     "mm_comm_init", "mm_comm_destroy", "mm_mixed_gemm_bf16_nshard_allgather",
@@ -103,6 +105,16 @@ def lib(build_if_missing: bool = False):
             "mm_gather_layout_words": (i64, [i32]),
             "mm_plan_set_gather_layout": (ctypes.c_int, [P, vp, vp]),
             "mm_gather_layout_host": (ctypes.c_int, [i32, ctypes.POINTER(i32), vp, vp]),
+            "mm_mc_supported": (i32, []),
+            "mm_mc_handle_bytes": (i32, []),
+            "mm_mc_window_create": (ctypes.c_int, [i32, i32, i64, i64, vp, ctypes.POINTER(vp)]),
+            "mm_mc_window_bind": (ctypes.c_int, [vp]),
+            "mm_mc_window_local": (vp, [vp]),
+            "mm_mc_window_set_timeout": (ctypes.c_int, [vp, ctypes.c_double]),
+            "mm_mc_window_error": (ctypes.c_int, [vp, ctypes.POINTER(i32)]),
+            "mm_mc_window_close": (ctypes.c_int, [vp]),
+            "mm_mc_barrier": (ctypes.c_int, [vp, vp]),
+            "mm_mixed_gemm_bf16_nshard_nvls": (ctypes.c_int, [X, X, P, i64, vp, i32, vp]),
             "mm_gather_wavefronts": (i64, [i32, ctypes.POINTER(i32), vp, vp]),
             "mm_reorder_act_bf16": (ctypes.c_int, [vp, i64, i64, P, vp, i64, vp]),
             "mm_set_gemm_config": (ctypes.c_int, [i32, i32, i32]),
@@ -505,3 +517,76 @@ def mm_mixed_gemm_bf16_nshard_peerstore(a: MXTensor, w_shard: MXTensor, plan: Pl
 
 def mm_peer_barrier(win: PeerWindow, stream=None):
     _check(lib().mm_peer_barrier(win.h, _stream(stream)))
+
+
+# ---- fused all-gather over NVLS (multicast; include/mm.h) ---------------------------
+def mc_supported() -> bool:
+    return bool(lib().mm_mc_supported())
+
+
+class McWindow:
+    """This rank's view of a multicast object spanning every rank's [Y][flags] buffer.
+    create() is collective over the torch process group (world 1 without one)."""
+
+    def __init__(self, h, rank, world, M, ldy):
+        self.h, self.rank, self.world, self.M, self.ldy = h, rank, world, M, ldy
+
+    @classmethod
+    def create(cls, M: int, ldy: int, group=None):
+        import torch.distributed as dist
+        dist_on = dist.is_available() and dist.is_initialized()
+        rank = dist.get_rank(group) if dist_on else 0
+        world = dist.get_world_size(group) if dist_on else 1
+        rec = ctypes.create_string_buffer(lib().mm_mc_handle_bytes())
+        h = ctypes.c_void_p()
+        if rank == 0:
+            _check(lib().mm_mc_window_create(0, world, M, ldy, rec, ctypes.byref(h)))
+        if world > 1:
+            obj = [rec.raw if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            if rank != 0:
+                rec = ctypes.create_string_buffer(obj[0], len(obj[0]))
+                _check(lib().mm_mc_window_create(rank, world, M, ldy, rec, ctypes.byref(h)))
+            dist.barrier(group)                 # every device added before any bind
+        _check(lib().mm_mc_window_bind(h))
+        if world > 1:
+            dist.barrier(group)                 # every buffer bound and zeroed before use
+        return cls(h, rank, world, M, ldy)
+
+    def y(self) -> torch.Tensor:
+        """This rank's Y [M, ldy] (BF16) as a torch view of the window's local buffer."""
+        ptr = lib().mm_mc_window_local(self.h)
+        n = self.M * self.ldy
+        return _from_ptr(ptr, n, torch.bfloat16).view(self.M, self.ldy)
+
+    def set_timeout(self, seconds: float):
+        _check(lib().mm_mc_window_set_timeout(self.h, float(seconds)))
+
+    def timed_out(self) -> bool:
+        v = ctypes.c_int32()
+        _check(lib().mm_mc_window_error(self.h, ctypes.byref(v)))
+        return bool(v.value)
+
+    def close(self):
+        if self.h is not None:
+            _check(lib().mm_mc_window_close(self.h))
+            self.h = None
+
+
+def _from_ptr(ptr: int, numel: int, dtype) -> torch.Tensor:
+    """A torch tensor over device memory the library owns (no copy; valid while it lives)."""
+    class _Cai:
+        def __init__(self):
+            self.__cuda_array_interface__ = {"shape": (numel,), "typestr": "<i2", "data": (ptr, False),
+                                             "version": 3, "strides": None}
+    return torch.as_tensor(_Cai(), device="cuda").view(dtype)
+
+
+def mm_mixed_gemm_bf16_nshard_nvls(a: MXTensor, w_shard: MXTensor, plan: Plan, n_total: int, win: McWindow,
+                                   barrier: bool = True, stream=None):
+    _check(lib().mm_mixed_gemm_bf16_nshard_nvls(ctypes.byref(a.c), ctypes.byref(w_shard.c), ctypes.byref(plan.c),
+                                                n_total, win.h, int(barrier), _stream(stream)))
+
+
+def mm_mc_barrier(win: McWindow, stream=None):
+    _check(lib().mm_mc_barrier(win.h, _stream(stream)))

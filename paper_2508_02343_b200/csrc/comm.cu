@@ -58,7 +58,42 @@ __global__ void peer_barrier_kernel(PeerFlags fl, int rank, int world, uint32_t 
   }
 }
 
+// NVLS barrier (NEXT F1 over NVLink SHARP): one system-scope release-add through the
+// multicast view increments word 0 of EVERY rank's flag array; each rank then waits for
+// its own copy to reach world * epoch.  The preceding GEMM's multimem stores are
+// performed first (kernel boundary + system fence + release).
+__global__ void mc_barrier_kernel(uint32_t* flags_mc, uint32_t* flags_local, int world, uint32_t epoch,
+                                  uint64_t timeout_ns) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(flags_mc), "r"(1u) : "memory");
+  const uint32_t target = (uint32_t)world * epoch;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags_local) : "memory");
+    if ((int32_t)(v - target) >= 0) break;
+    if (timeout_ns) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicCAS(flags_local + kPeerErrSlot, 0u, 0xFFFFu);   // some rank(s) missing
+        return;
+      }
+    }
+    __nanosleep(100);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_mc_barrier(uint32_t* flags_mc, uint32_t* flags_local, int world, uint32_t epoch,
+                              uint64_t timeout_ns, cudaStream_t s, int64_t* launches) {
+  mc_barrier_kernel<<<1, 32, 0, s>>>(flags_mc, flags_local, world, epoch, timeout_ns);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_peer_barrier(const PeerFlags& fl, int rank, int world, uint32_t epoch, uint64_t timeout_ns,
                                 cudaStream_t s, int64_t* launches) {

@@ -408,7 +408,7 @@ static GemmPath choose_path(const GemmArgs& a, const GemmConfig& cfg) {
   int bn = cfg.block_n;
   // auto: CTA-pair 256 x 256 tiles once M fills a pair tile's rows, else single-CTA 128 x 256
   if (bn == 0) bn = a.M > 128 ? 512 : 256;
-  if (a.n_dst > 0) return PATH_PAIR;   // the fused all-gather epilogue lives in the CTA-pair kernel
+  if (a.n_dst > 0 || a.y_mc) return PATH_PAIR;   // the fused all-gather epilogues live in the CTA-pair kernel
   // small M (decode-like): swap-AB + split-K kernel (gemm_sm.cu), unless a tile
   // configuration is forced, MM_GEMM_SMALLM=0, or the caller's path must not use a
   // workspace (N-shard entry points).

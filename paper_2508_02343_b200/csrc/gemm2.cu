@@ -80,6 +80,8 @@ struct Gemm2Dev {
   int ndst;  // output maps used (1, or the peer window's world size)
   int raster;  // pair-row blocks per raster group (8; MM_GEMM_RASTER for tuning)
   int helpers; // 1: warps 0-3 drain half of the LAST tile's accumulator (data-parallel schedule)
+  uint16_t* y_mc;        // NVLS: multicast view of all ranks' Y (nullptr: TMA stores)
+  int64_t mc_col_off;    // this rank's column offset in the full Y
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
 };
 
@@ -516,6 +518,23 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         uint32_t w[16];
 #pragma unroll
         for (int v = 0; v < 16; ++v) w[v] = ptx::pack_bf16x2(__uint_as_float(r[2 * v]), __uint_as_float(r[2 * v + 1]));
+        if (p.y_mc) {
+          // NVLS: row row0 + lane, 32 columns as four 16-byte multimem stores (one write
+          // per element reaches every rank's Y); rows >= M and columns >= N (the shard)
+          // are clipped like the TMA boxes clip them.
+          const int64_t rr = row0 + lane;
+          const int col = n0 + 32 * c;
+          if (rr < M) {
+            uint16_t* dst = p.y_mc + rr * p.ldy + p.mc_col_off + col;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (col + 8 * k < N)
+                asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(dst + 8 * k),
+                             "r"(w[4 * k]), "r"(w[4 * k + 1]), "r"(w[4 * k + 2]), "r"(w[4 * k + 3])
+                             : "memory");
+          }
+          continue;
+        }
         uint8_t* buf = stg + (nstore % NB) * 2048;
         if (lane == 0) ptx::bulk_wait_group_read<NB - 1>();   // the store that last used `buf` has read it
         __syncwarp();
@@ -676,6 +695,8 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.y = a.y;
   p.ldy = a.ldy;
   p.ndst = ndst;
+  p.y_mc = a.y_mc;
+  p.mc_col_off = a.y_col_off;
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
   { const char* r = getenv("MM_GEMM_RASTER"); p.raster = (r && atoi(r) > 0) ? atoi(r) : 8; }
   if (p.num_tiles == 0) return cudaSuccess;
@@ -688,7 +709,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   {
     const char* h = getenv("MM_GEMM_HELPERS");
     const bool want = h ? atoi(h) == 1 : p.num_tiles <= 4 * npairs;
-    p.helpers = (!p.stream_k && want) ? 1 : 0;
+    p.helpers = (!p.stream_k && !p.y_mc && want) ? 1 : 0;
   }
   if (p.stream_k) {   // caller workspace: [flags npairs x 8 ints, 256-B padded][partials]
     if (!a.ws || a.ws_bytes < pair_workspace_bytes(a, cfg)) {

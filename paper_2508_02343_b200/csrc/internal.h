@@ -79,6 +79,9 @@ struct GemmArgs {
   int n_dst = 0;
   uint16_t* y_dst[8] = {};
   int64_t y_col_off = 0;
+  // Fused all-gather over NVLS (multicast): y_mc != nullptr stores every output element
+  // with multimem.st into the multicast view of all ranks' Y (columns + y_col_off).
+  uint16_t* y_mc = nullptr;
   // Caller-owned GEMM workspace (split-K partials / stream-K partials + flags),
   // zero-filled before its first use; the kernels leave every counter at zero.
   void* ws = nullptr;
@@ -114,6 +117,10 @@ struct PeerFlags {
   uint32_t* f[kMaxPeers];
 };
 constexpr int kPeerErrSlot = 63;   // flag-array word holding a barrier timeout (missing rank + 1)
+// NVLS barrier: every rank adds 1 to word 0 of the multicast flag array (all ranks' copies)
+// and waits until its own copy reaches world * epoch (comm.cu).
+cudaError_t launch_mc_barrier(uint32_t* flags_mc, uint32_t* flags_local, int world, uint32_t epoch,
+                              uint64_t timeout_ns, cudaStream_t s, int64_t* launches);
 cudaError_t launch_peer_barrier(const PeerFlags& fl, int rank, int world, uint32_t epoch, uint64_t timeout_ns,
                                 cudaStream_t s, int64_t* launches);
 

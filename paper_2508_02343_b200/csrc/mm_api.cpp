@@ -11,6 +11,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <sys/syscall.h>
+#include <unistd.h>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -544,7 +546,8 @@ static GemmConfig current_cfg() {
 // point without a workspace argument (N-shard): never pick a path that needs one.
 static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const mm_plan* plan, void* d_y,
                              int64_t ldy, int64_t n_cols, mm_stream_t stream, void* d_ws, size_t ws_bytes,
-                             bool no_ws, const MmPeerWin* win = nullptr) {
+                             bool no_ws, const MmPeerWin* win = nullptr, uint16_t* y_mc = nullptr,
+                             int64_t mc_col_off = 0) {
   mm_status st = check_device();
   if (st != MM_OK) return st;
   if ((st = validate_plan(plan)) != MM_OK) return st;
@@ -575,6 +578,10 @@ static mm_status gemm_common(const mm_mx_tensor* a, const mm_mx_tensor* w, const
     ga.n_dst = win->world;
     for (int r = 0; r < win->world; ++r) ga.y_dst[r] = win->y[r];
     ga.y_col_off = (int64_t)win->rank * N;
+  }
+  if (y_mc) {   // NVLS: the multicast view of the full Y; this rank's columns start at mc_col_off
+    ga.y_mc = y_mc;
+    ga.y_col_off = mc_col_off;
   }
   GemmConfig cfg = current_cfg();
   cfg.no_stream_k = cfg.no_stream_k || no_ws;
@@ -814,6 +821,307 @@ mm_status mm_peer_window_error(void* win, int32_t* h_missing_rank) {
   cudaError_t e = cudaMemcpy(&v, w->flags[w->rank] + kPeerErrSlot, sizeof(v), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "reading the peer error word");
   *h_missing_rank = (int32_t)v - 1;
+  return MM_OK;
+}
+
+// ---------------------------------------------------------------- NVLS (multicast) window
+// NEXT F1 over NVLink SHARP: one multicast object spans every rank's Y buffer; the GEMM
+// epilogue writes each output element ONCE with multimem.st and the NVSwitch replicates
+// it to all ranks (per-GPU egress (G-1)x smaller than storing to each peer).  Built on
+// the driver's virtual-memory API (resolved at run time; no libcuda link).
+struct CuVmm {
+  decltype(&cuMulticastCreate) mcCreate = nullptr;
+  decltype(&cuMulticastAddDevice) mcAddDevice = nullptr;
+  decltype(&cuMulticastBindMem) mcBindMem = nullptr;
+  decltype(&cuMulticastUnbind) mcUnbind = nullptr;
+  decltype(&cuMulticastGetGranularity) mcGranularity = nullptr;
+  decltype(&cuMemCreate) memCreate = nullptr;
+  decltype(&cuMemRelease) memRelease = nullptr;
+  decltype(&cuMemAddressReserve) addrReserve = nullptr;
+  decltype(&cuMemAddressFree) addrFree = nullptr;
+  decltype(&cuMemMap) memMap = nullptr;
+  decltype(&cuMemUnmap) memUnmap = nullptr;
+  decltype(&cuMemSetAccess) setAccess = nullptr;
+  decltype(&cuMemExportToShareableHandle) exportHandle = nullptr;
+  decltype(&cuMemImportFromShareableHandle) importHandle = nullptr;
+  decltype(&cuMemGetAllocationGranularity) allocGranularity = nullptr;
+  decltype(&cuDeviceGet) deviceGet = nullptr;
+  decltype(&cuDeviceGetAttribute) deviceAttr = nullptr;
+  bool ok = false;
+};
+static const CuVmm& cuvmm() {
+  static CuVmm api;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    auto get = [](const char* name) -> void* {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      return (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+              q == cudaDriverEntryPointSuccess) ? p : nullptr;
+    };
+    api.mcCreate = reinterpret_cast<decltype(api.mcCreate)>(get("cuMulticastCreate"));
+    api.mcAddDevice = reinterpret_cast<decltype(api.mcAddDevice)>(get("cuMulticastAddDevice"));
+    api.mcBindMem = reinterpret_cast<decltype(api.mcBindMem)>(get("cuMulticastBindMem"));
+    api.mcUnbind = reinterpret_cast<decltype(api.mcUnbind)>(get("cuMulticastUnbind"));
+    api.mcGranularity = reinterpret_cast<decltype(api.mcGranularity)>(get("cuMulticastGetGranularity"));
+    api.memCreate = reinterpret_cast<decltype(api.memCreate)>(get("cuMemCreate"));
+    api.memRelease = reinterpret_cast<decltype(api.memRelease)>(get("cuMemRelease"));
+    api.addrReserve = reinterpret_cast<decltype(api.addrReserve)>(get("cuMemAddressReserve"));
+    api.addrFree = reinterpret_cast<decltype(api.addrFree)>(get("cuMemAddressFree"));
+    api.memMap = reinterpret_cast<decltype(api.memMap)>(get("cuMemMap"));
+    api.memUnmap = reinterpret_cast<decltype(api.memUnmap)>(get("cuMemUnmap"));
+    api.setAccess = reinterpret_cast<decltype(api.setAccess)>(get("cuMemSetAccess"));
+    api.exportHandle = reinterpret_cast<decltype(api.exportHandle)>(get("cuMemExportToShareableHandle"));
+    api.importHandle = reinterpret_cast<decltype(api.importHandle)>(get("cuMemImportFromShareableHandle"));
+    api.allocGranularity = reinterpret_cast<decltype(api.allocGranularity)>(get("cuMemGetAllocationGranularity"));
+    api.deviceGet = reinterpret_cast<decltype(api.deviceGet)>(get("cuDeviceGet"));
+    api.deviceAttr = reinterpret_cast<decltype(api.deviceAttr)>(get("cuDeviceGetAttribute"));
+    api.ok = api.mcCreate && api.mcAddDevice && api.mcBindMem && api.mcUnbind && api.mcGranularity &&
+             api.memCreate && api.memRelease && api.addrReserve && api.addrFree && api.memMap && api.memUnmap &&
+             api.setAccess && api.exportHandle && api.importHandle && api.allocGranularity && api.deviceGet &&
+             api.deviceAttr;
+  });
+  return api;
+}
+
+// Shareable handle record exchanged by the caller (mm_mc_handle_bytes() bytes).
+struct McHandleRec {
+  uint32_t type;       // 0: none (world 1), 1: fabric handle, 2: POSIX fd (imported with pidfd_getfd)
+  uint32_t pid;
+  int32_t fd;
+  uint32_t pad;
+  uint8_t fabric[64];
+};
+
+struct MmMcWin {
+  int rank = 0, world = 0, dev = 0;
+  int64_t M = 0, ldy = 0;
+  size_t bytes = 0;                      // mapped size (granularity-rounded)
+  CUmemGenericAllocationHandle mc = 0, mem = 0;
+  CUdeviceptr mc_va = 0, local_va = 0;
+  bool bound = false;
+  int exported_fd = -1;
+  uint32_t epoch = 0;
+  uint64_t timeout_ns = 0;
+};
+
+static mm_status cu_fail(CUresult r, const char* what) { return fail(MM_ERR_CUDA, "%s: CUresult %d", what, (int)r); }
+
+int32_t mm_mc_handle_bytes(void) { return (int32_t)sizeof(McHandleRec); }
+
+int32_t mm_mc_supported(void) {
+  const CuVmm& api = cuvmm();
+  if (!api.ok) return 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  CUdevice cd;
+  if (api.deviceGet(&cd, dev) != CUDA_SUCCESS) return 0;
+  int v = 0;
+  if (api.deviceAttr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cd) != CUDA_SUCCESS || !v) return 0;
+  // The attribute is not enough: a box whose GPU is not attached to an NVSwitch fabric
+  // rejects cuMulticastCreate (CUDA_ERROR_INVALID_VALUE).  Probe once per device.
+  static std::mutex mu;
+  static int probed[64] = {0};   // 0 unknown, 1 yes, 2 no
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 0 && dev < 64 && probed[dev]) return probed[dev] == 1;
+  CUmulticastObjectProp mp{};
+  mp.numDevices = 1;
+  size_t g = 0;
+  mp.size = 2u << 20;
+  if (api.mcGranularity(&g, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS && g > mp.size) mp.size = g;
+  CUmemGenericAllocationHandle h = 0;
+  const bool ok = api.mcCreate(&h, &mp) == CUDA_SUCCESS;
+  if (ok) api.memRelease(h);
+  if (dev >= 0 && dev < 64) probed[dev] = ok ? 1 : 2;
+  return ok ? 1 : 0;
+}
+
+mm_status mm_mc_window_create(int32_t rank, int32_t world, int64_t M, int64_t ldy, void* h_handle, void** win_out) {
+  mm_status st = peer_window_check(rank, world, M, ldy);
+  if (st != MM_OK) return st;
+  if (!win_out || (world > 1 && !h_handle)) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  const CuVmm& api = cuvmm();
+  if (!api.ok) return fail(MM_ERR_CUDA, "driver virtual-memory / multicast entry points unavailable");
+  if (!mm_mc_supported()) return fail(MM_ERR_UNSUPPORTED_DEVICE, "device does not support multicast objects");
+  MmMcWin* w = new MmMcWin;
+  w->rank = rank;
+  w->world = world;
+  w->M = M;
+  w->ldy = ldy;
+  cudaGetDevice(&w->dev);
+  CUdevice cd;
+  api.deviceGet(&cd, w->dev);
+  // size: [Y][64 flags], rounded to both granularities
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = w->dev;
+  size_t ag = 0, mg = 0;
+  CUmulticastObjectProp mp{};
+  mp.numDevices = (unsigned)world;
+  mp.size = mm_peer_buffer_bytes(M, ldy);
+  CUresult r = api.allocGranularity(&ag, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+  if (r == CUDA_SUCCESS) r = api.mcGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED);
+  if (r != CUDA_SUCCESS) { delete w; return cu_fail(r, "granularity"); }
+  const size_t g = std::max(ag, mg);
+  w->bytes = (mp.size + g - 1) / g * g;
+  mp.size = w->bytes;
+  McHandleRec* rec = static_cast<McHandleRec*>(h_handle);
+  if (rank == 0) {
+    // fabric handles first (IMEX), else a POSIX fd the peers duplicate with pidfd_getfd
+    const CUmemAllocationHandleType types[2] = {CU_MEM_HANDLE_TYPE_FABRIC, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR};
+    bool done = false;
+    for (int k = 0; k < (world > 1 ? 2 : 1) && !done; ++k) {
+      mp.handleTypes = world > 1 ? (unsigned long long)types[k] : 0ull;
+      if (api.mcCreate(&w->mc, &mp) != CUDA_SUCCESS) continue;
+      if (world == 1) { done = true; break; }
+      McHandleRec out{};
+      out.pid = (uint32_t)getpid();
+      out.fd = -1;
+      if (types[k] == CU_MEM_HANDLE_TYPE_FABRIC) {
+        CUmemFabricHandle fh;
+        if (api.exportHandle(&fh, w->mc, CU_MEM_HANDLE_TYPE_FABRIC, 0) == CUDA_SUCCESS) {
+          out.type = 1;
+          std::memcpy(out.fabric, fh.data, sizeof(out.fabric));
+          done = true;
+        }
+      } else {
+        int fd = -1;
+        if (api.exportHandle(&fd, w->mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) == CUDA_SUCCESS) {
+          out.type = 2;
+          out.fd = fd;
+          w->exported_fd = fd;
+          done = true;
+        }
+      }
+      if (done) *rec = out;
+      else { api.memRelease(w->mc); w->mc = 0; }
+    }
+    if (!done) { delete w; return fail(MM_ERR_CUDA, "cuMulticastCreate / export of the multicast handle failed"); }
+  } else {
+    if (rec->type == 1) {
+      CUmemFabricHandle fh;
+      std::memcpy(fh.data, rec->fabric, sizeof(rec->fabric));
+      r = api.importHandle(&w->mc, &fh, CU_MEM_HANDLE_TYPE_FABRIC);
+    } else if (rec->type == 2) {
+      const int pidfd = (int)syscall(434 /* SYS_pidfd_open */, (int)rec->pid, 0);
+      const int fd = pidfd >= 0 ? (int)syscall(438 /* SYS_pidfd_getfd */, pidfd, rec->fd, 0) : -1;
+      if (pidfd >= 0) close(pidfd);
+      if (fd < 0) { delete w; return fail(MM_ERR_CUDA, "pidfd_getfd of the multicast handle failed"); }
+      r = api.importHandle(&w->mc, reinterpret_cast<void*>((uintptr_t)fd), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+      close(fd);
+    } else {
+      delete w;
+      return fail(MM_ERR_INVALID_ARGUMENT, "bad multicast handle record");
+    }
+    if (r != CUDA_SUCCESS) { delete w; return cu_fail(r, "import multicast handle"); }
+  }
+  r = api.mcAddDevice(w->mc, cd);
+  if (r != CUDA_SUCCESS) { api.memRelease(w->mc); delete w; return cu_fail(r, "cuMulticastAddDevice"); }
+  *win_out = w;
+  return MM_OK;
+}
+
+mm_status mm_mc_window_bind(void* win) {
+  if (!win) return fail(MM_ERR_INVALID_ARGUMENT, "NULL window");
+  MmMcWin* w = static_cast<MmMcWin*>(win);
+  if (w->bound) return MM_OK;
+  const CuVmm& api = cuvmm();
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = w->dev;
+  CUresult r = api.memCreate(&w->mem, w->bytes, &ap, 0);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuMemCreate");
+  r = api.mcBindMem(w->mc, 0, w->mem, 0, w->bytes, 0);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuMulticastBindMem");
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = w->dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  r = api.addrReserve(&w->local_va, w->bytes, 0, 0, 0);
+  if (r == CUDA_SUCCESS) r = api.memMap(w->local_va, w->bytes, 0, w->mem, 0);
+  if (r == CUDA_SUCCESS) r = api.setAccess(w->local_va, w->bytes, &acc, 1);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "map the local buffer");
+  r = api.addrReserve(&w->mc_va, w->bytes, 0, 0, 0);
+  if (r == CUDA_SUCCESS) r = api.memMap(w->mc_va, w->bytes, 0, w->mc, 0);
+  if (r == CUDA_SUCCESS) r = api.setAccess(w->mc_va, w->bytes, &acc, 1);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "map the multicast view");
+  cudaError_t e = cudaMemset(reinterpret_cast<void*>(w->local_va), 0, w->bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "zero the window");
+  w->bound = true;
+  return MM_OK;
+}
+
+void* mm_mc_window_local(void* win) {
+  return win ? reinterpret_cast<void*>(static_cast<MmMcWin*>(win)->local_va) : nullptr;
+}
+
+mm_status mm_mc_window_set_timeout(void* win, double seconds) {
+  if (!win || !(seconds >= 0.0)) return fail(MM_ERR_INVALID_ARGUMENT, "NULL window or negative timeout");
+  static_cast<MmMcWin*>(win)->timeout_ns = (uint64_t)(seconds * 1e9);
+  return MM_OK;
+}
+
+mm_status mm_mc_window_error(void* win, int32_t* h_timed_out) {
+  if (!win || !h_timed_out) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  MmMcWin* w = static_cast<MmMcWin*>(win);
+  if (!w->bound) return fail(MM_ERR_INVALID_ARGUMENT, "window not bound");
+  uint32_t v = 0;
+  cudaError_t e = cudaMemcpy(&v, reinterpret_cast<uint32_t*>(w->local_va + peer_y_bytes(w->M, w->ldy)) + kPeerErrSlot,
+                             sizeof(v), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "reading the window error word");
+  *h_timed_out = v ? 1 : 0;
+  return MM_OK;
+}
+
+mm_status mm_mc_window_close(void* win) {
+  if (!win) return MM_OK;
+  MmMcWin* w = static_cast<MmMcWin*>(win);
+  const CuVmm& api = cuvmm();
+  cudaDeviceSynchronize();
+  if (w->mc_va) { api.memUnmap(w->mc_va, w->bytes); api.addrFree(w->mc_va, w->bytes); }
+  if (w->local_va) { api.memUnmap(w->local_va, w->bytes); api.addrFree(w->local_va, w->bytes); }
+  CUdevice cd;
+  api.deviceGet(&cd, w->dev);
+  if (w->bound) api.mcUnbind(w->mc, cd, 0, w->bytes);
+  if (w->mem) api.memRelease(w->mem);
+  if (w->mc) api.memRelease(w->mc);
+  if (w->exported_fd >= 0) close(w->exported_fd);
+  delete w;
+  return MM_OK;
+}
+
+mm_status mm_mc_barrier(void* win, mm_stream_t stream) {
+  if (!win) return fail(MM_ERR_INVALID_ARGUMENT, "NULL window");
+  MmMcWin* w = static_cast<MmMcWin*>(win);
+  if (!w->bound) return fail(MM_ERR_INVALID_ARGUMENT, "window not bound (mm_mc_window_bind)");
+  const size_t yb = peer_y_bytes(w->M, w->ldy);
+  uint32_t* f_mc = reinterpret_cast<uint32_t*>(w->mc_va + yb);
+  uint32_t* f_loc = reinterpret_cast<uint32_t*>(w->local_va + yb);
+  const uint32_t epoch = ++w->epoch;
+  cudaError_t e = launch_mc_barrier(f_mc, f_loc, w->world, epoch, w->timeout_ns, reinterpret_cast<cudaStream_t>(stream),
+                                    &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "NVLS barrier launch");
+  return MM_OK;
+}
+
+mm_status mm_mixed_gemm_bf16_nshard_nvls(const mm_mx_tensor* a, const mm_mx_tensor* w_shard, const mm_plan* plan,
+                                         int64_t n_total, void* win, int32_t barrier, mm_stream_t stream) {
+  if (!win || !a || !w_shard) return fail(MM_ERR_INVALID_ARGUMENT, "NULL argument");
+  MmMcWin* w = static_cast<MmMcWin*>(win);
+  if (!w->bound) return fail(MM_ERR_INVALID_ARGUMENT, "window not bound (mm_mc_window_bind)");
+  const int64_t Ns = w_shard->rows;
+  if (Ns * w->world != n_total) return fail(MM_ERR_SHAPE, "shard rows * world != n_total");
+  if (Ns % 16 != 0) return fail(MM_ERR_SHAPE, "shard rows must be a multiple of 16");
+  if (a->rows != w->M) return fail(MM_ERR_SHAPE, "activation rows %lld != window M %lld", (long long)a->rows, (long long)w->M);
+  if (w->ldy < n_total) return fail(MM_ERR_SHAPE, "window ldy < n_total");
+  uint16_t* y_loc = reinterpret_cast<uint16_t*>(w->local_va);
+  mm_status st = gemm_common(a, w_shard, plan, y_loc + (int64_t)w->rank * Ns, w->ldy, Ns, stream, nullptr, 0,
+                             /*no_ws=*/true, nullptr, reinterpret_cast<uint16_t*>(w->mc_va), (int64_t)w->rank * Ns);
+  if (st != MM_OK) return st;
+  if (barrier) return mm_mc_barrier(win, stream);
   return MM_OK;
 }
 

@@ -9,6 +9,8 @@ replicated activation's reorder-quantize and then
     exchanged through the torch process group), and
   * mm_mixed_gemm_bf16_nshard_peerstore (fused all-gather epilogue: every tile
     TMA-stored into every rank's Y over CUDA-IPC peer mappings, flag barrier),
+  * mm_mixed_gemm_bf16_nshard_nvls (the same through one multicast object: each
+    element written once with multimem.st, replicated by the switch) where supported,
 and checks both gathered outputs (a) bit-equal to the 1-GPU GEMM of the full W on
 its own device (each element's K order does not depend on the N offset, DESIGN.md
 §8) and (b) against the fp64 oracle on sampled rows (tests/accuracy.py bars)."""
@@ -68,6 +70,18 @@ def _worker(rank, world, port, M, N, n, q):
             win.close()
         ok_nccl = torch.equal(y_nccl.view(torch.int16), y_full.view(torch.int16))
         ok_peer = torch.equal(y_peer.view(torch.int16), y_full.view(torch.int16))
+        if mm.mc_supported():   # NVLS: multimem stores through a multicast object over all ranks
+            mwin = mm.McWindow.create(M, N)
+            try:
+                mwin.set_timeout(60.0)
+                for _ in range(2):
+                    mm.mm_mixed_gemm_bf16_nshard_nvls(a, w_shard, plan, N, mwin, barrier=True)
+                torch.cuda.synchronize()
+                dist.barrier()
+                ok_peer = ok_peer and torch.equal(mwin.y().view(torch.int16), y_full.view(torch.int16)) \
+                    and not mwin.timed_out()
+            finally:
+                mwin.close()
         rep = None
         if rank == 0:
             import sys
