@@ -173,6 +173,10 @@ def dist_init():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        # NCCL's init log shows the N ranks (kept off stdout, which carries the JSON line)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -392,6 +396,7 @@ def run_gpu(args, rank, world, local):
     nshard = args.config == "llama70b_down" and (world > 1 or args.comm == "peer")
     use_peer = nshard and args.comm == "peer"
     comm = win = y_peer = None
+    fused_err = None
     if nshard:
         from paper_2508_02343_b200.dist import exchange_unique_id
         comm = mm.mm_comm_init(rank, world, exchange_unique_id(mm.nccl_unique_id)) if world > 1 else \
@@ -400,10 +405,17 @@ def run_gpu(args, rank, world, local):
         # fused all-gather epilogue: tiles stored into every rank's Y over NVLink
         if world > 1:
             from paper_2508_02343_b200.dist import open_peer_window
-            win, y_peer = open_peer_window(M, N)
+            try:
+                win, y_peer = open_peer_window(M, N)   # collective; fails on every rank together
+            except RuntimeError as e_:
+                if use_peer:
+                    raise
+                win, y_peer, fused_err = None, None, str(e_)
         else:
             buf = mm.peer_buffer(M, N, device=dev)
             win, y_peer = mm.PeerWindow.from_ptrs(0, 1, [buf], M, N), mm.peer_y(buf, M, N)
+    if win is not None:
+        win.set_timeout(60.0)   # a rank that never arrives must not hang the box
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     # bytes touched per step (for the L2 rotation count)
     Ns = N // world if nshard else N
@@ -484,8 +496,14 @@ def run_gpu(args, rank, world, local):
                 "allgather_bytes": 2 * M * N,
                 "allgather_note": "torch.distributed all_gather_into_tensor (NCCL) of the same BF16 bytes, "
                                   "busbw = (G-1)/G x bytes / time"}
+            mwin, nvls_err = None, None
             if mm.mc_supported():   # NVLS: each element written once via multimem.st, switch replicates
-                mwin = mm.McWindow.create(M, N)
+                try:
+                    mwin = mm.McWindow.create(M, N)   # collective; fails on every rank together
+                    mwin.set_timeout(60.0)
+                except mm.MMError as e_:
+                    nvls_err = str(e_)
+            if mwin is not None:
                 try:
                     def nvls_step(i):
                         st_ = sets[i % n_sets]
@@ -508,7 +526,9 @@ def run_gpu(args, rank, world, local):
                     barrier(world)
                     mwin.close()
             else:
-                extra_nshard["nvls_allgather"] = "unavailable: this GPU cannot create multicast objects"
+                extra_nshard["nvls_allgather"] = "unavailable: " + (nvls_err or "this GPU cannot create multicast objects")
+            if win is None:
+                extra_nshard["fused_allgather"] = "unavailable: " + (fused_err or "not run")
             if win is not None:   # the fused all-gather epilogue on the same ranks
                 barrier(world)
                 torch.cuda.synchronize()
@@ -683,9 +703,7 @@ def relaunch_under_torchrun(n):
     sk.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-    env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")    # NCCL's init log shows the N ranks
-    sys.exit(subprocess.call(cmd, env=env))
+    sys.exit(subprocess.call(cmd, env=dict(os.environ)))
 
 
 def main():

@@ -539,18 +539,39 @@ class McWindow:
         world = dist.get_world_size(group) if dist_on else 1
         rec = ctypes.create_string_buffer(lib().mm_mc_handle_bytes())
         h = ctypes.c_void_p()
-        if rank == 0:
-            _check(lib().mm_mc_window_create(0, world, M, ldy, rec, ctypes.byref(h)))
+        err = ""
+
+        def agree(ok: bool):
+            """Every rank learns whether all ranks succeeded (no rank is left waiting)."""
+            if world == 1:
+                return ok
+            t = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                             device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            return bool(t.item())
+
+        st = lib().mm_mc_window_create(0, world, M, ldy, rec, ctypes.byref(h)) if rank == 0 else 0
+        if st != 0:
+            err = lib().mm_last_error().decode()
         if world > 1:
-            obj = [rec.raw if rank == 0 else None]
+            obj = [rec.raw if (rank == 0 and st == 0) else None]
             dist.broadcast_object_list(obj, src=0, group=group)
-            if rank != 0:
+            if rank != 0 and obj[0] is not None:
                 rec = ctypes.create_string_buffer(obj[0], len(obj[0]))
-                _check(lib().mm_mc_window_create(rank, world, M, ldy, rec, ctypes.byref(h)))
-            dist.barrier(group)                 # every device added before any bind
-        _check(lib().mm_mc_window_bind(h))
-        if world > 1:
-            dist.barrier(group)                 # every buffer bound and zeroed before use
+                st = lib().mm_mc_window_create(rank, world, M, ldy, rec, ctypes.byref(h))
+                if st != 0:
+                    err = lib().mm_last_error().decode()
+            elif rank != 0:
+                st, err = 7, "rank 0 could not create the multicast object"
+        if not agree(st == 0):                  # every device added before any bind
+            if h.value:
+                lib().mm_mc_window_close(h)
+            raise MMError(7, "multicast window: " + (err or "another rank failed"))
+        st = lib().mm_mc_window_bind(h)
+        err = "" if st == 0 else lib().mm_last_error().decode()
+        if not agree(st == 0):                  # every buffer bound and zeroed before use
+            lib().mm_mc_window_close(h)
+            raise MMError(7, "multicast window bind: " + (err or "another rank failed"))
         return cls(h, rank, world, M, ldy)
 
     def y(self) -> torch.Tensor:

@@ -71,5 +71,18 @@ def open_peer_window(M: int, ldy: int, group=None):
     buf = mm.peer_buffer(M, ldy)
     torch.cuda.synchronize()
     handles = exchange_handles(mm.ipc_handle(buf), group)
-    win = mm.PeerWindow.open(rank, world, buf, handles, M, ldy)
+    win, err = None, ""
+    try:
+        win = mm.PeerWindow.open(rank, world, buf, handles, M, ldy)
+    except mm.MMError as e:
+        err = str(e)
+    # every rank learns whether every rank mapped its peers: nobody may enter a barrier
+    # that a rank without a window would never join
+    t = torch.tensor([0 if win is None else 1], dtype=torch.int32,
+                     device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    if not int(t.item()):
+        if win is not None:
+            win.close()
+        raise RuntimeError("peer window: " + (err or "another rank could not map its peers"))
     return win, mm.peer_y(buf, M, ldy)
