@@ -3,13 +3,15 @@
 // caption line 148; Eq. 1 lines 40-45), sm_100a.
 //
 // HBM-bound streaming kernel (see rq_kernel below for the tile structure):
-//   * R rows at a time are streamed from HBM with 128-bit loads and written into
-//     shared memory "row-interleaved": smem slot p holds the R BF16 values of
-//     channel p (R = 2: 4-byte slots), XOR-swizzled so the 128-bit -> slot
-//     transposition stores are bank-conflict free;
-//   * a thread owns one 32-channel block of the reordered row: the gather
+//   * tiles of R rows are streamed from HBM by TMA into a shared-memory ring and
+//     transposed in place into "row-interleaved" slots: slot p holds the R BF16
+//     values of channel p (R = 2: 4-byte slots); the transpose's 16-byte chunk
+//     stores are ordered to be bank-conflict free, and an optional plan-time gather
+//     layout (layout.cpp) permutes the 4-channel chunks inside each 128-byte line;
+//   * a lane pair owns one 32-channel block of the reordered row: the gather
 //     x_r[j] = X[perm[j]] is a single shared load per channel that fetches all R
-//     rows at once (R-fold fewer random smem accesses than a per-row gather);
+//     rows at once (R-fold fewer random smem accesses than a per-row gather), its
+//     slot offsets read from a per-plan table built once per CTA;
 //     block amax is an integer max over |bf16| bits; the E8M0
 //     exponent is integer arithmetic on the BF16 exponent field (no log2f); the
 //     scaled value x * 2^-e is exact (power of two, no FTZ); the element code is
@@ -112,25 +114,6 @@ template <int R> struct Slot;
 template <> struct Slot<1> { using T = uint16_t; };
 template <> struct Slot<2> { using T = uint32_t; };
 template <> struct Slot<4> { using T = uint2; };
-
-// Shared-memory slot load at a 32-bit shared address (the gather: stage base, a
-// uniform register, + a per-lane table offset -> one LDS [R + UR]).
-template <typename ST> __device__ __forceinline__ ST lds_slot(uint32_t addr);
-template <> __device__ __forceinline__ uint16_t lds_slot<uint16_t>(uint32_t addr) {
-  uint16_t v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
-  return v;
-}
-template <> __device__ __forceinline__ uint32_t lds_slot<uint32_t>(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
-}
-template <> __device__ __forceinline__ uint2 lds_slot<uint2>(uint32_t addr) {
-  uint2 v;
-  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
-  return v;
-}
 
 // Row RHO of a slot as an fp32 value (BF16 = the top half of an fp32).
 template <int RHO>
