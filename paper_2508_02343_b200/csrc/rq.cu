@@ -247,13 +247,19 @@ __device__ __forceinline__ void norm_slot(uint2& v, uint32_t gbits, const float 
 
 // Block amax of each of the R rows over |bf16| bits (packed 16x2 maxima).  With
 // NV = 16 each lane holds half a block; the lane pair combines with one shuffle.
+template <int NV, typename F>
+__device__ __forceinline__ uint32_t tree_reduce(const uint32_t (&w)[NV], F f);
+__device__ __forceinline__ uint32_t absmax_bf16x2(uint32_t a, uint32_t b);
 template <int NV>
 __device__ __forceinline__ void block_amax(const uint16_t (&v)[NV], uint32_t (&am)[4]) {
-  uint32_t m = 0;
+  // single-row slots: pack channel pairs into bf16x2 words (one PRMT per pair) and
+  // reduce them with the packed |max| -- half the operations of a per-value max
+  uint32_t w[NV / 2];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) m = max(m, uint32_t(v[i]) & 0x7FFFu);
-  if constexpr (NV == 16) m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
-  am[0] = m;
+  for (int i = 0; i < NV / 2; ++i) w[i] = __byte_perm(uint32_t(v[2 * i]), uint32_t(v[2 * i + 1]), 0x5410);
+  uint32_t m = tree_reduce<NV / 2>(w, absmax_bf16x2);
+  if constexpr (NV == 16) m = absmax_bf16x2(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  am[0] = max(m & 0x7FFFu, (m >> 16) & 0x7FFFu);
 }
 // max(|a|, |b|) per BF16 half (sign = xor of the signs; masked off by the caller):
 // one instruction per word instead of an abs-mask and an integer max.  Inputs are
