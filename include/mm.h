@@ -216,9 +216,10 @@ mm_status mm_rmsnorm_reorder_quantize_act(const void* d_x, int64_t M, int64_t ld
  * (fingerprints equal) -- else MM_ERR_PLAN_MISMATCH.  N % 16 == 0.
  * Small M (<= 128 when the W tiles leave room for >= 2 K splits) runs the swap-AB /
  * split-K kernel: each K split keeps its own FP32 accumulator and the partials are
- * added in split order (deterministic; reading R28).  Its FP32 partials
- * and arrival counters (and those of the opt-in stream-K schedule) live in the
- * CALLER's workspace d_ws of ws_bytes >= mm_gemm_workspace_bytes(plan, M, N) bytes:
+ * added in split order (deterministic; reading R28) inside the thread-block
+ * cluster of the split CTAs (distributed shared memory; no workspace).  The opt-in
+ * stream-K schedule's FP32 partials and flags live in the CALLER's workspace d_ws of
+ * ws_bytes >= mm_gemm_workspace_bytes(plan, M, N) bytes:
  * 256-byte aligned, ZERO-FILLED once before its first use (the kernels leave every
  * counter at zero), reusable by later calls on the same stream, not shared by calls
  * in flight on different streams.  d_ws may be NULL when the query returns 0.

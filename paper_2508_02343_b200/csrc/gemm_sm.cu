@@ -45,8 +45,6 @@ struct SmDev {
   uint32_t idesc[3];
   uint16_t* y;
   int64_t ldy;
-  float* ws;             // [num_nt * splits][BNM][128] FP32 partials (splits > 1)
-  int* cnt;              // [num_nt] arrival counters (left at zero)
   int interleave;        // 1: units take every splits-th stage, 0: contiguous K ranges (default; measured equal)
   int dbg;
 };
@@ -103,7 +101,6 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-  __shared__ int s_last;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const bool trace = (p.dbg & 32) && blockIdx.x < 1024;
@@ -232,51 +229,66 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
         }
       }
     } else {
-      // 1) this unit's FP32 partial -> workspace [unit][m][128] (coalesced over lanes)
-      float* mine = p.ws + (size_t)blockIdx.x * BNM * 128;
+      // this unit's FP32 partial -> its own shared memory [m][128] (the operand ring is
+      // idle once tfull completed: every MMA has read its stages)
+      float* part = reinterpret_cast<float*>(sW);
 #pragma unroll 1
       for (int c = 0; c < BNM / 32; ++c) {
+        if (32 * c >= M) break;
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + 32 * c, r);
         ptx::tc_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) __stcg(mine + (size_t)(32 * c + j) * 128 + nl, __uint_as_float(r[j]));
+        for (int j = 0; j < 32; ++j)
+          if (32 * c + j < M) part[(32 * c + j) * 128 + nl] = __uint_as_float(r[j]);
       }
-      // 2) arrival: the last unit of this W tile reduces all partials in split order
       if (trace && q == 0 && lane == 0) g_sm_trace[blockIdx.x][5] = ptx::globaltimer_ns();
-      __threadfence();
-      ptx::named_bar_sync(1, 128);
-      if (warp == 4 && lane == 0) {
-        const int prev = atomicAdd(p.cnt + nt, 1);
-        s_last = prev == p.splits - 1;
-        if (s_last) p.cnt[nt] = 0;   // re-arm for the next launch (nobody else touches it now)
-      }
-      ptx::named_bar_sync(1, 128);
-      if (s_last) {
-        __threadfence();
-        const float* base = p.ws + (size_t)nt * p.splits * BNM * 128;
-        if (n < p.N) {
-          // 8 rows x up to kMaxSplits partials in flight per thread; summed in split order
+    }
+  }
+
+  if (p.splits > 1) {
+    // Split-K reduction inside the thread-block cluster of this W tile (cluster rank =
+    // split index): after a cluster barrier, the epilogue warps of every split read the
+    // partials of their share of the rows from all splits' shared memory (DSMEM), add
+    // them in split order (the deterministic order of DESIGN.md R28) and round once to
+    // BF16.  A second barrier keeps every CTA's shared memory alive until all reads are
+    // done.  No global workspace and no arrival counters.
+    ptx::cluster_sync();
+    if (warp >= 4) {
+      // every CTA of the cluster reduces the rows m = ks, ks + splits, ...: 8 rows x
+      // up to kMaxSplits remote loads in flight per thread, summed in split order
+      const int nl = (warp & 3) * 32 + lane;
+      const int64_t n = (int64_t)nt * 128 + nl;
+      const int M = (int)p.M;
+      if (n < p.N) {
+        const uint32_t base = ptx::smem_u32(sW) + 4u * (uint32_t)nl;
 #pragma unroll 1
-          for (int m0 = 0; m0 < M; m0 += 8) {
-            float v[8][kMaxSplits];
+        for (int m0 = ks; m0 < M; m0 += 8 * p.splits) {
+          float v[8][kMaxSplits];
 #pragma unroll
-            for (int mm = 0; mm < 8; ++mm)
+          for (int mm = 0; mm < 8; ++mm)
 #pragma unroll
-              for (int k2 = 0; k2 < kMaxSplits; ++k2)
-                v[mm][k2] = (m0 + mm < M && k2 < p.splits) ? __ldcg(base + ((size_t)k2 * BNM + m0 + mm) * 128 + nl) : 0.f;
-#pragma unroll
-            for (int mm = 0; mm < 8; ++mm) {
-              float acc = v[mm][0];
-#pragma unroll
-              for (int k2 = 1; k2 < kMaxSplits; ++k2)
-                if (k2 < p.splits) acc += v[mm][k2];
-              if (m0 + mm < M) p.y[(int64_t)(m0 + mm) * p.ldy + n] = (uint16_t)(ptx::pack_bf16x2(acc, 0.f) & 0xFFFFu);
+            for (int k2 = 0; k2 < kMaxSplits; ++k2) {
+              const int m = m0 + mm * p.splits;
+              v[mm][k2] = 0.f;
+              if (m < M && k2 < p.splits) {
+                const uint32_t ra = ptx::mapa(base + 512u * (uint32_t)m, (uint32_t)k2);
+                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v[mm][k2]) : "r"(ra) : "memory");
+              }
             }
+#pragma unroll
+          for (int mm = 0; mm < 8; ++mm) {
+            const int m = m0 + mm * p.splits;
+            float acc = v[mm][0];
+#pragma unroll
+            for (int k2 = 1; k2 < kMaxSplits; ++k2)
+              if (k2 < p.splits) acc += v[mm][k2];
+            if (m < M) p.y[(int64_t)m * p.ldy + n] = (uint16_t)(ptx::pack_bf16x2(acc, 0.f) & 0xFFFFu);
           }
         }
       }
     }
+    ptx::cluster_sync();
   }
 
   ptx::tc_fence_before();
@@ -287,8 +299,8 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
 }
 
 // Split count of the small-M kernel: fill the SMs once (one CTA per SM), at least 2
-// stages per unit, at most kMaxSplits (the last unit's reduction reads splits x M x
-// 512 B per tile).
+// stages per unit, at most kMaxSplits (the splits of a tile form one cluster; split 0
+// reads splits x M x 512 B of partials from its peers' shared memory).
 int sm_splits(const GemmArgs& a, const GemmConfig& cfg) {
   const int num_nt = (int)((a.N + 127) / 128);
   int S = (a.geom.kp[0] + 255) / 256 + a.geom.kp[1] / 128 + a.geom.kp[2] / 128;
@@ -305,15 +317,9 @@ int sm_bnm(int64_t M) { return M <= 32 ? 32 : (M <= 64 ? 64 : 128); }
 
 }  // namespace
 
-// Caller workspace of the small-M kernel: [arrival counters: one int per 128-row W
-// tile, 256-B padded][FP32 partials: tiles x splits x BNM x 128].  Zero-filled once by
-// the caller; the last unit of a tile re-arms its counter.
-size_t smallm_workspace_bytes(const GemmArgs& a, const GemmConfig& cfg) {
-  const int splits = sm_splits(a, cfg);
-  if (splits <= 1) return 0;
-  const size_t num_nt = (size_t)((a.N + 127) / 128);
-  return ws_align(num_nt * sizeof(int)) + num_nt * splits * sm_bnm(a.M) * 128 * sizeof(float);
-}
+// The small-M kernel needs no workspace: its split-K partials are reduced inside a
+// thread-block cluster through distributed shared memory.
+size_t smallm_workspace_bytes(const GemmArgs&, const GemmConfig&) { return 0; }
 
 namespace {
 
@@ -356,18 +362,18 @@ cudaError_t run_sm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int
   (void)S;
   const int splits = sm_splits(a, cfg);
   p.splits = splits;
-  if (splits > 1) {   // caller workspace (size checked by the API layer before any launch)
-    const size_t need = smallm_workspace_bytes(a, cfg);
-    if (!a.ws || a.ws_bytes < need) { *err = "split-K workspace missing or too small"; return cudaErrorInvalidValue; }
-    p.cnt = static_cast<int*>(a.ws);
-    p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a.ws) + ws_align((size_t)p.num_nt * sizeof(int)));
-  }
+
   const size_t smem = 1024 + (size_t)STAGES * C::STAGE_BYTES + (2 * STAGES + 1) * 8 + 16;
   auto kern = mixgemm_sm_kernel<BNM, STAGES>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
-  e = launch_pdl(kern, dim3(p.num_nt * splits), dim3(kThreadsSm), smem, s, maps[0], maps[1], maps[2], maps[3],
-                 maps[4], maps[5], p);
+  // the splits of one W tile form a thread-block cluster (cluster rank = split index)
+  if (splits > 1)
+    e = launch_pdl_cluster(kern, dim3(p.num_nt * splits), dim3(kThreadsSm), smem, s, splits, maps[0], maps[1],
+                           maps[2], maps[3], maps[4], maps[5], p);
+  else
+    e = launch_pdl(kern, dim3(p.num_nt * splits), dim3(kThreadsSm), smem, s, maps[0], maps[1], maps[2], maps[3],
+                   maps[4], maps[5], p);
   if (launches) ++*launches;
   return e != cudaSuccess ? e : cudaGetLastError();
 }

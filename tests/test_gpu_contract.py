@@ -1,7 +1,8 @@
 """GPU checks of the boundary contract of include/mm.h: the hot calls
-allocate nothing and never synchronize -- the GEMM's split-K / stream-K partials
-live in a caller workspace sized by mm_gemm_workspace_bytes -- so the small-M
-(decode) path can be captured into a CUDA graph; errors are reported before any
+allocate nothing and never synchronize -- the small-M split-K partials are reduced
+inside a thread-block cluster, the opt-in stream-K partials live in a caller
+workspace sized by mm_gemm_workspace_bytes -- so the small-M (decode) path can be
+captured into a CUDA graph; errors are reported before any
 launch; a peer barrier whose peer never arrives reports instead of trapping."""
 import numpy as np
 import pytest
@@ -22,23 +23,22 @@ def _ops(M, N, n, seed=51):
     return plan, a, w
 
 
-def test_workspace_query_matches_paths():
+def test_workspace_query_matches_paths(monkeypatch):
     plan, _, _ = _ops(16, 4096, (2240, 1184, 672))
-    assert mm.mm_gemm_workspace_bytes(plan, 16, 4096) > 0        # small-M split-K
+    assert mm.mm_gemm_workspace_bytes(plan, 16, 4096) == 0       # small-M split-K: reduced in a cluster (DSMEM)
     assert mm.mm_gemm_workspace_bytes(plan, 2048, 4096) == 0     # CTA-pair tiles
     assert mm.mm_gemm_workspace_bytes(plan, 0, 4096) == 0
-    mm.mm_set_gemm_config(256, 0, 0)                            # forced tile kernel: none
-    try:
-        assert mm.mm_gemm_workspace_bytes(plan, 16, 4096) == 0
-    finally:
-        mm.mm_set_gemm_config(0, 0, 0)
+    monkeypatch.setenv("MM_GEMM_STREAMK", "1")                  # stream-K: 80 tiles on 74 pairs -> partials
+    assert mm.mm_gemm_workspace_bytes(plan, 2048, 2560) > 0
 
 
-def test_workspace_too_small_is_an_error_and_enqueues_nothing():
-    plan, a, w = _ops(16, 4096, (2240, 1184, 672))
-    need = mm.mm_gemm_workspace_bytes(plan, 16, 4096)
+def test_workspace_too_small_is_an_error_and_enqueues_nothing(monkeypatch):
+    monkeypatch.setenv("MM_GEMM_STREAMK", "1")
+    plan, a, w = _ops(2048, 2560, (2240, 1184, 672))
+    need = mm.mm_gemm_workspace_bytes(plan, 2048, 2560)
+    assert need > 0
     ws = torch.zeros(need - 256, dtype=torch.uint8, device="cuda")
-    y = torch.full((16, 4096), 7.0, dtype=torch.bfloat16, device="cuda")
+    y = torch.full((2048, 2560), 7.0, dtype=torch.bfloat16, device="cuda")
     n0 = mm.launch_count()
     with pytest.raises(mm.MMError) as e:
         mm.mm_mixed_gemm_bf16(a, w, plan, out=y, workspace=ws)
@@ -58,8 +58,7 @@ def test_small_m_gemm_captured_in_cuda_graph(M):
     wq = mm.mm_quantize_weight_offline(gen_weight(N, K, 3000).cuda(), plan)
     x_static = gen_act(M, K, 1000, 2100).cuda()
     s = torch.cuda.Stream()
-    ws = mm.gemm_workspace(plan, M, N, stream=s)          # allocated before the capture
-    assert ws is not None
+    ws = mm.gemm_workspace(plan, M, N, stream=s)          # (none needed: cluster split-K reduction)
     a = mm.MXTensor(plan, M, x_static.device)
     y = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     s.wait_stream(torch.cuda.current_stream())
