@@ -677,8 +677,9 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
           // parity-preserving gather layout (an odd chunk stays odd: still 8 bank groups
           // per store instruction)
           int p0 = 2 * (lane & 3), p1 = p0 + 1;
-          if (layout) {
-            const uint32_t lw = lay_s[8 * b + (lane >> 2)];
+          const int li = 8 * b + (lane >> 2);   // 32-channel line of this lane's chunks
+          if (layout && li < K / 32) {          // lines past K (the last box's OOB tail) stay natural
+            const uint32_t lw = lay_s[li];
             p0 = (lw >> (4 * p0)) & 7;
             p1 = (lw >> (4 * p1)) & 7;
           }

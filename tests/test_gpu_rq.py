@@ -180,7 +180,8 @@ def test_rmsnorm_rejects_bad_eps():
         mm.mm_rmsnorm_reorder_quantize_act(x, g, 0.0, plan)
 
 
-@pytest.mark.parametrize("K,n", [(4096, (2240, 1184, 672)), (14336, (8512, 3840, 1984))])
+@pytest.mark.parametrize("K,n", [(4096, (2240, 1184, 672)), (14336, (8512, 3840, 1984)), (480, (96, 160, 224)),
+                                 (800, (320, 256, 224))])
 def test_gather_layout_does_not_change_results(K, n):
     """The plan-time gather layout (mm_plan_set_gather_layout) only moves values inside
     shared memory: codes and scales equal those of the natural layout, byte for byte,
