@@ -762,6 +762,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       if (e4m3) seg_chunks<R, NORM, 2, F_E4M3>(a, cx, cf2, rn);
       else seg_chunks<R, NORM, 2, F_E5M2>(a, cx, cf2, rn);
       if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][3 + 2 * i] = ptx::globaltimer_ns();
+      if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && gw == 0 && lane == 0) g_rq_trace[blockIdx.x][15] = ptx::globaltimer_ns();
       // ---- release the stage (every warp of the group arrives once) ----
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s]));

@@ -119,3 +119,29 @@ def test_peer_barrier_timeout_reports_missing_rank():
         assert float(z.sum()) == 12.0
     finally:
         w0.close()
+
+
+@pytest.mark.parametrize("M", [16, 2048])
+def test_gemm_sees_weights_quantized_just_before(M):
+    """The GEMMs load W before their griddepcontrol.wait (W prefetch): correct only
+    because mm_quantize_weight_offline never releases its dependents early.  Re-quantize
+    DIFFERENT weights into the same buffer right before each GEMM (and an activation RQ in
+    between or not): every GEMM must see the new W."""
+    N, n = 4096, (2240, 1184, 672)
+    K = sum(n)
+    plan = mm.mm_plan_init(K, n, gen_perm(K, 53))
+    a = mm.mm_reorder_quantize_act(gen_act(M, K, 1000, 2400).cuda(), plan)
+    w_buf = mm.MXTensor(plan, N, torch.device("cuda"))
+    ys = []
+    for i in range(3):
+        mm.mm_quantize_weight_offline(gen_weight(N, K, 3100 + i).cuda(), plan, out=w_buf)
+        if i == 2:   # RQ of A between the weight quantization and the GEMM
+            a = mm.mm_reorder_quantize_act(gen_act(M, K, 1000, 2400).cuda(), plan, out=a)
+        ys.append(mm.mm_mixed_gemm_bf16(a, w_buf, plan))
+    torch.cuda.synchronize()
+    for i in range(3):
+        wq = mm.mm_quantize_weight_offline(gen_weight(N, K, 3100 + i).cuda(), plan)
+        torch.cuda.synchronize()
+        y_ref = mm.mm_mixed_gemm_bf16(a, wq, plan)
+        torch.cuda.synchronize()
+        assert torch.equal(ys[i].view(torch.int16), y_ref.view(torch.int16)), i
