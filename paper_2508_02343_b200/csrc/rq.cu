@@ -383,7 +383,9 @@ __device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& c
     const bool live = kb_raw < nb;                 // pair-uniform
     const int kb = live ? kb_raw : nb - 1;
     const bool pad = kb * 32 >= n || (cx.dbg & 8);
-    const int kbg = pad ? 0 : kb;                  // block whose channels are gathered
+    // block whose channels are gathered (timing experiment 64: always block 0, i.e. a
+    // conflict-free broadcast gather with the full encode)
+    const int kbg = pad || (MM_RQ_EXPERIMENTS && (cx.dbg & 64)) ? 0 : kb;
     uint8_t* crow0 = crow_base + (unsigned)kb * (2 * hb);
     uint8_t* sfp = sf_base + ((unsigned)kb >> 2) * 512 + (kb & 3);
     if (MM_RQ_EXPERIMENTS && (cx.dbg & 16)) continue;   // timing experiment: no stores at all
