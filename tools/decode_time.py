@@ -1,5 +1,6 @@
-"""Decode-shape GEMM timing (small-M kernel): q_proj / down at M = 1..128, rotating
-weights > L2, CUDA events.  python tools/decode_time.py"""
+"""Decode-shape timing (small-M kernel): q_proj / down at M = 1..128, rotating weights
+> L2, CUDA events: the GEMM alone back to back, and the step (RQ of the activation +
+GEMM) back to back.  python tools/decode_time.py"""
 import os
 import sys
 
@@ -17,10 +18,17 @@ for K, N in ((4096, 4096), (14336, 4096)):
     plan = sc.calibrated_plan(K, layer=0)
     nset = max(2, min(16, -(-3 * L2 // (N * K))))
     ws = [mm.mm_quantize_weight_offline(gen_weight(N, K, 3000 + i, device="cuda"), plan) for i in range(nset)]
-    res = []
+    res, res_step = [], []
     for M in (1, 16, 32, 64, 128):
-        a = mm.mm_reorder_quantize_act(gen_act(M, K, 1000, 2001, device="cuda"), plan)
+        x = gen_act(M, K, 1000, 2001, device="cuda")
+        a = mm.mm_reorder_quantize_act(x, plan)
         y = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         us = sc.time_loop(lambda i: mm.mm_mixed_gemm_bf16(a, ws[i], plan, out=y), nset, 40)
         res.append(f"M={M}:{us:.2f}us")
-    print(f"K={K} N={N} " + " ".join(res), flush=True)
+
+        def step(i):
+            mm.mm_reorder_quantize_act(x, plan, out=a)
+            mm.mm_mixed_gemm_bf16(a, ws[i], plan, out=y)
+        res_step.append(f"M={M}:{sc.time_loop(step, nset, 40):.2f}us")
+    print(f"K={K} N={N} gemm " + " ".join(res), flush=True)
+    print(f"K={K} N={N} step " + " ".join(res_step), flush=True)
