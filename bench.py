@@ -617,10 +617,20 @@ def run_gpu(args, rank, world, local):
         win.close()
 
     large = None
+    large_more = []
     if world == 1 and args.large and args.config == "q_proj":
         M3, K3, N3 = 16384, 14336, 4096
         large = measure_shape(M3, K3, N3, dev, stream, pk, layer=1)
         large["workload"] = "Llama-3.1-8B down_proj at batch 8 x seq 2048 (BASELINE configs[2], b8 down)"
+        # the other BASELINE shapes the driver can observe on one GPU: b8 q/o (configs[2])
+        # and the north-star 70B down_proj unsharded (configs[3] at N = 1)
+        for (Mx, Kx, Nx, layer, what) in ((16384, 4096, 4096, 2, "Llama-3.1-8B q/o_proj at batch 8 x seq 2048 "
+                                                                  "(BASELINE configs[2], b8 q/o)"),
+                                          (8192, 28672, 8192, 3, "Llama-3.1-70B down_proj, 1 GPU (BASELINE "
+                                                                 "configs[3] unsharded)")):
+            r = measure_shape(Mx, Kx, Nx, dev, stream, pk, layer=layer)
+            r["workload"] = what
+            large_more.append(r)
 
     if rank != 0:
         return
@@ -690,6 +700,8 @@ def run_gpu(args, rank, world, local):
         out["nshard"] = extra_nshard
     if large is not None:
         out["large_shape"] = large
+    if large_more:
+        out["more_shapes"] = large_more
     print(json.dumps(out), flush=True)
 
 
