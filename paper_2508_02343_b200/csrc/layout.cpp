@@ -21,21 +21,18 @@ std::vector<uint32_t> gather_layout(int K, const int n[3], const int32_t* perm) 
   const int nlines = K / 32;
   std::vector<uint8_t> pos(K / 4);                 // chunk -> position in its line
   for (int c = 0; c < K / 4; ++c) pos[c] = (uint8_t)(c & 7);
-  // the kernel's gather steps: 32 channels per (segment, chunk, step q)
+  // the kernel's gather steps (rq.cu tile_chunks): chunk c, step q, lane l reads
+  // reordered position 32 b + 16 (l & 1) + q of block b = 16 c + l / 2 (dead lanes past
+  // the last block compute on the last block)
   std::vector<int32_t> steps;                       // [S][32]
-  int off = 0;
-  for (int g = 0; g < 3; ++g) {
-    const int kp = (n[g] + 127) / 128 * 128, nb = kp / 32, nch = (nb + 15) / 16;
-    for (int c = 0; c < nch; ++c)
-      for (int q = 0; q < 16; ++q)
-        for (int l = 0; l < 32; ++l) {
-          const int kb_raw = 16 * c + l / 2;
-          const int kb = kb_raw < nb ? kb_raw : nb - 1;     // dead lanes compute on the last block
-          const int kbg = kb * 32 >= n[g] ? 0 : kb;         // padding blocks gather block 0
-          steps.push_back(perm[off + 32 * kbg + 16 * (l & 1) + q]);
-        }
-    off += n[g];
-  }
+  const int nbt = K / 32, nch = (nbt + 15) / 16;
+  (void)n;
+  for (int c = 0; c < nch; ++c)
+    for (int q = 0; q < 16; ++q)
+      for (int l = 0; l < 32; ++l) {
+        const int b = std::min(16 * c + l / 2, nbt - 1);
+        steps.push_back(perm[32 * b + 16 * (l & 1) + q]);
+      }
   const int S = (int)steps.size() / 32;
   if (S == 0) return std::vector<uint32_t>(nlines, 0x76543210u);
   // steps touching each line
@@ -101,29 +98,24 @@ std::vector<uint32_t> gather_layout(int K, const int n[3], const int32_t* perm) 
 
 // Total gather wavefronts of a layout (diagnostics / tests): natural layout = nullptr.
 long long gather_wavefronts(int K, const int n[3], const int32_t* perm, const uint32_t* layout) {
+  (void)n;
   long long tot = 0;
-  int off = 0;
-  for (int g = 0; g < 3; ++g) {
-    const int kp = (n[g] + 127) / 128 * 128, nb = kp / 32, nch = (nb + 15) / 16;
-    for (int c = 0; c < nch; ++c)
-      for (int q = 0; q < 16; ++q) {
-        int cnt[32] = {0}, seen[32], ns = 0, best = 0;
-        for (int l = 0; l < 32; ++l) {
-          const int kb_raw = 16 * c + l / 2;
-          const int kb = kb_raw < nb ? kb_raw : nb - 1;
-          const int kbg = kb * 32 >= n[g] ? 0 : kb;
-          const int p = perm[off + 32 * kbg + 16 * (l & 1) + q];
-          bool dup = false;
-          for (int i = 0; i < ns; ++i) dup |= seen[i] == p;
-          if (dup) continue;
-          seen[ns++] = p;
-          const int ps = layout ? (int)((layout[p >> 5] >> (4 * ((p >> 2) & 7))) & 7) : ((p >> 2) & 7);
-          best = std::max(best, ++cnt[(4 * ps + (p & 3)) & 31]);
-        }
-        tot += best;
+  const int nbt = K / 32, nch = (nbt + 15) / 16;
+  for (int c = 0; c < nch; ++c)
+    for (int q = 0; q < 16; ++q) {
+      int cnt[32] = {0}, seen[32], ns = 0, best = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int b = std::min(16 * c + l / 2, nbt - 1);
+        const int p = perm[32 * b + 16 * (l & 1) + q];
+        bool dup = false;
+        for (int i = 0; i < ns; ++i) dup |= seen[i] == p;
+        if (dup) continue;
+        seen[ns++] = p;
+        const int ps = layout ? (int)((layout[p >> 5] >> (4 * ((p >> 2) & 7))) & 7) : ((p >> 2) & 7);
+        best = std::max(best, ++cnt[(4 * ps + (p & 3)) & 31]);
       }
-    off += n[g];
-  }
+      tot += best;
+    }
   return tot;
 }
 

@@ -327,21 +327,21 @@ __device__ __forceinline__ void quantize_row(const ST (&v)[NV], uint32_t amax, i
   }
 }
 
+// Rows of one block after its amax is known (no warp-collective operations, so it
+// may run under divergence: a chunk that straddles two segments runs two formats).
 template <int R, int G, int FMT, int NV>
-__device__ __forceinline__ void quantize_tile_block(const typename Slot<R>::T (&v)[NV], int off, uint8_t* crow0,
-                                                    int64_t pitch, uint8_t* sfp, int nvalid, bool live, bool store_sf,
-                                                    bool zero) {
-  uint32_t am[4];
-  block_amax<NV>(v, am);   // every lane of the warp (full-warp shuffle)
-  quantize_row<0, G, FMT, NV>(v, am[0], off, crow0, sfp, live && nvalid > 0, store_sf, zero);
-  if constexpr (R >= 2) quantize_row<1, G, FMT, NV>(v, am[1], off, crow0 + pitch, sfp, live && nvalid > 1, store_sf, zero);
+__device__ __forceinline__ void quantize_rows(const typename Slot<R>::T (&v)[NV], const uint32_t (&am)[4], int off,
+                                              uint8_t* crow0, uint32_t pitch, uint8_t* sfp, int nvalid, bool live,
+                                              bool store_sf) {
+  quantize_row<0, G, FMT, NV>(v, am[0], off, crow0, sfp, live && nvalid > 0, store_sf, false);
+  if constexpr (R >= 2) quantize_row<1, G, FMT, NV>(v, am[1], off, crow0 + pitch, sfp, live && nvalid > 1, store_sf, false);
   if constexpr (R >= 4) {
-    quantize_row<2, G, FMT, NV>(v, am[2], off, crow0 + 2 * pitch, sfp, live && nvalid > 2, store_sf, zero);
-    quantize_row<3, G, FMT, NV>(v, am[3], off, crow0 + 3 * pitch, sfp, live && nvalid > 3, store_sf, zero);
+    quantize_row<2, G, FMT, NV>(v, am[2], off, crow0 + 2 * pitch, sfp, live && nvalid > 2, store_sf, false);
+    quantize_row<3, G, FMT, NV>(v, am[3], off, crow0 + 3 * pitch, sfp, live && nvalid > 3, store_sf, false);
   }
 }
 
-// Per-tile context of a consumer warp (everything seg_chunks needs besides the plan).
+// Per-tile context of a consumer warp (everything tile_chunks needs besides the plan).
 template <int R> struct ChunkCtx {
   const uint8_t* st;        // stage: 256-channel boxes of row-interleaved slots
   const uint8_t* smem0;     // shared-memory base (the stage's offset from it is made warp-uniform)
@@ -354,44 +354,40 @@ template <int R> struct ChunkCtx {
   int tab;
 };
 
-// The chunks of segment G owned by this warp (local chunk c_first, c_first +
-// group_warps, ...) for one tile: gather, (norm), block amax, E8M0 scale, encode,
-// store.  G is a compile-time constant, so the segment's geometry is read straight
-// from the kernel parameters (uniform registers, no per-chunk selects).
-template <int R, bool NORM, int G, int FMT>
-__device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& cx, int c_first, const float (&rn)[4]) {
+__device__ __forceinline__ int sel3(int g, int x0, int x1, int x2) { return g == 0 ? x0 : (g == 1 ? x1 : x2); }
+
+// The chunks of one tile owned by this warp (chunk c_first, c_first + group_warps, ...).
+// A chunk is 16 consecutive 32-channel blocks of the REORDERED row -- the segments are
+// contiguous there (FP4 blocks, then FP6, then FP8) -- so a K = 4096 row is 8 chunks
+// whatever the mix (per-segment chunks would need 10 at the q_proj mix, two of them
+// two-thirds idle).  The lane pair (2 l, 2 l + 1) owns block 16 c + l: gather, (norm),
+// block amax and the E8M0 exponent run on every lane; the encode + stores branch on the
+// block's segment, which is warp-uniform except in the (at most two) chunks that
+// straddle a segment boundary.  Storage padding blocks (n_g .. kp_g) are written by
+// tile_padding.
+template <int R, bool NORM>
+__device__ __forceinline__ void tile_chunks(const RqArgs& a, const ChunkCtx<R>& cx, int c_first, bool e3m2,
+                                            bool e4m3, const float (&rn)[4]) {
   using ST = typename Slot<R>::T;
-  const int kp = a.geom.kp[G], nb = (unsigned)kp >> 5, nch = (unsigned)(nb + 15) >> 4;
+  const int nbt = (unsigned)a.K >> 5;                           // real blocks of the row
+  const int nch = (unsigned)(nbt + 15) >> 4;
   if (c_first >= nch) return;
-  const int n = a.geom.n[G], segoff = a.geom.off[G], sco = a.geom.sc_off[G];
-  const uint32_t pitch = (uint32_t)a.geom.pitch[G];   // < 2^32 (K <= 65536)
-  const int h = cx.lane & 1;                       // which half of the block
-  constexpr int hb = G == 0 ? 8 : (G == 1 ? 12 : 16);   // code bytes per half block
+  const int b1 = (unsigned)a.geom.off[1] >> 5, b2 = (unsigned)a.geom.off[2] >> 5;   // first block of FP6 / FP8
+  const int h = cx.lane & 1;                                    // which half of the block
   const unsigned r0 = (unsigned)cx.r0;
-  // the stage base through a warp reduction: a uniform register, so every gather load
-  // is one LDS [R + UR] with no per-slot address add
   const uint32_t st_off = __reduce_max_sync(0xffffffffu, (uint32_t)(cx.st - cx.smem0));
   const uint8_t* const st_u = cx.smem0 + st_off;
-  uint8_t* const crow_base = a.codes[G] + (uint64_t)r0 * pitch + h * hb;
-  uint8_t* const sf_base = a.sf[G] + (size_t)((r0 >> 7) * ((unsigned)kp >> 7)) * 512 + (r0 & 31) * 16 + ((r0 >> 5) & 3) * 4;
-  // The chunk loop is warp-uniform and every lane runs the whole block path (the
-  // block amax combines the lane pair with a full-warp shuffle): lanes past the
-  // segment's last block compute on a valid block and store nothing; padding blocks
-  // (past n) gather block 0 and store zero codes and zero scale bytes.
+  // per-tile row bases of the three segments' code rows and scale atoms
+  const unsigned sf_row = (r0 & 31) * 16 + ((r0 >> 5) & 3) * 4;
   for (int c = c_first; c < nch; c += cx.group_warps) {
-    const int kb_raw = c * 16 + (cx.lane >> 1);
-    const bool live = kb_raw < nb;                 // pair-uniform
-    const int kb = live ? kb_raw : nb - 1;
-    const bool pad = kb * 32 >= n || (cx.dbg & 8);
-    // block whose channels are gathered (timing experiment 64: always block 0, i.e. a
-    // conflict-free broadcast gather with the full encode)
-    const int kbg = pad || (MM_RQ_EXPERIMENTS && (cx.dbg & 64)) ? 0 : kb;
-    uint8_t* crow0 = crow_base + (unsigned)kb * (2 * hb);
-    uint8_t* sfp = sf_base + ((unsigned)kb >> 2) * 512 + (kb & 3);
-    if (MM_RQ_EXPERIMENTS && (cx.dbg & 16)) continue;   // timing experiment: no stores at all
+    const int b_raw = c * 16 + (cx.lane >> 1);
+    const bool live = b_raw < nbt;                              // pair-uniform
+    const int b = live ? b_raw : nbt - 1;                       // dead lanes compute on the last block
+    if (MM_RQ_EXPERIMENTS && (cx.dbg & 16)) continue;           // timing experiment: no stores at all
+    const int bg = (MM_RQ_EXPERIMENTS && (cx.dbg & 64)) ? 0 : b;   // experiment 64: broadcast gather
     ST v[16];
     if (cx.tab == 3) {   // u32 offsets: 4 x 128-bit table loads, slot address = stage base + offset
-      const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + segoff + 32 * kbg + 16 * h);
+      const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + 32 * bg + 16 * h);
       const int rot = (cx.lane >> 1) & 3;          // the table build's per-lane rotation
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
@@ -402,7 +398,7 @@ __device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& c
         v[4 * q4 + 3] = *reinterpret_cast<const ST*>(st_u + e.w);
       }
     } else if (cx.tab) {
-      const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + 16 * ((segoff >> 5) + kbg) + 8 * h);
+      const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + 16 * bg + 8 * h);
       const int rot = (cx.lane >> 2) & 1;          // the table build's per-lane swap
       const uint4 p0 = gp[rot], p1 = gp[rot ^ 1];
       const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
@@ -413,7 +409,7 @@ __device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& c
       }
     } else {
       const ST* slots = reinterpret_cast<const ST*>(cx.st);
-      const int4* pp = reinterpret_cast<const int4*>(a.perm + segoff + 32 * kbg + 16 * h);
+      const int4* pp = reinterpret_cast<const int4*>(a.perm + 32 * bg + 16 * h);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int4 pv = __ldg(pp + q);
@@ -424,13 +420,59 @@ __device__ __forceinline__ void seg_chunks(const RqArgs& a, const ChunkCtx<R>& c
       }
     }
     if constexpr (NORM) {
-      const uint4* gp4 = reinterpret_cast<const uint4*>(cx.gamma_r + segoff + 32 * kbg + 16 * h);
+      const uint4* gp4 = reinterpret_cast<const uint4*>(cx.gamma_r + 32 * bg + 16 * h);
       const uint4 ga = gp4[0], gb = gp4[1];
       const uint32_t gw8[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
 #pragma unroll
       for (int i = 0; i < 16; ++i) norm_slot<R>(v[i], (gw8[i >> 1] >> (16 * (i & 1))) & 0xFFFFu, rn);
     }
-    quantize_tile_block<R, G, FMT, 16>(v, sco, crow0, pitch, sfp, cx.nvalid, live, live && h == 0, pad);
+    uint32_t am[4];
+    block_amax<16>(v, am);   // every lane of the warp (full-warp shuffle), before any divergence
+    const int g = b < b1 ? 0 : (b < b2 ? 1 : 2);
+    const int kb = b - sel3(g, 0, b1, b2);                      // block inside its segment
+    const int hb = sel3(g, 8, 12, 16);                          // code bytes per half block
+    const uint32_t pitch = (uint32_t)sel3(g, (int)a.geom.pitch[0], (int)a.geom.pitch[1], (int)a.geom.pitch[2]);
+    const int kp = sel3(g, a.geom.kp[0], a.geom.kp[1], a.geom.kp[2]);
+    const int off = sel3(g, a.geom.sc_off[0], a.geom.sc_off[1], a.geom.sc_off[2]);
+    uint8_t* const codes = g == 0 ? a.codes[0] : (g == 1 ? a.codes[1] : a.codes[2]);
+    uint8_t* const sf = g == 0 ? a.sf[0] : (g == 1 ? a.sf[1] : a.sf[2]);
+    uint8_t* crow0 = codes + (uint64_t)r0 * pitch + (unsigned)(h * hb) + (unsigned)kb * (2 * hb);
+    uint8_t* sfp = sf + (size_t)((r0 >> 7) * ((unsigned)kp >> 7) + ((unsigned)kb >> 2)) * 512 + sf_row + (kb & 3);
+    const bool store_sf = live && h == 0;
+    if (MM_RQ_EXPERIMENTS && (cx.dbg & 8)) continue;            // experiment: no encode, no stores
+    if (g == 0) {
+      quantize_rows<R, 0, F_E2M1, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
+    } else if (g == 1) {
+      if (e3m2) quantize_rows<R, 1, F_E3M2, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
+      else quantize_rows<R, 1, F_E2M3, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
+    } else {
+      if (e4m3) quantize_rows<R, 2, F_E4M3, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
+      else quantize_rows<R, 2, F_E5M2, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
+    }
+  }
+}
+
+// Storage padding of one tile: the blocks n_g .. kp_g of every segment (at most three
+// per segment) get zero codes (rows inside the matrix) and zero scale bytes (all R rows
+// of the tile).  One lane per (padding block, row).
+template <int R>
+__device__ __forceinline__ void tile_padding(const RqArgs& a, int r0, int nvalid, int lane) {
+  const int np0 = (a.geom.kp[0] - a.geom.n[0]) >> 5, np1 = (a.geom.kp[1] - a.geom.n[1]) >> 5;
+  const int tot = np0 + np1 + ((a.geom.kp[2] - a.geom.n[2]) >> 5);
+  for (int t = lane; t < tot * R; t += 32) {
+    const int rho = t % R, p = t / R;
+    const int g = p < np0 ? 0 : (p < np0 + np1 ? 1 : 2);
+    const int kb = (sel3(g, a.geom.n[0], a.geom.n[1], a.geom.n[2]) >> 5) + p - sel3(g, 0, np0, np0 + np1);
+    const int64_t r = (int64_t)r0 + rho;
+    const int hb2 = sel3(g, 16, 24, 32);   // code bytes per block
+    uint8_t* const codes = g == 0 ? a.codes[0] : (g == 1 ? a.codes[1] : a.codes[2]);
+    uint8_t* const sf = g == 0 ? a.sf[0] : (g == 1 ? a.sf[1] : a.sf[2]);
+    if (rho < nvalid) {
+      uint32_t* c = reinterpret_cast<uint32_t*>(codes + r * sel3(g, (int)a.geom.pitch[0], (int)a.geom.pitch[1],
+                                                               (int)a.geom.pitch[2]) + (int64_t)kb * hb2);
+      for (int w = 0; w < hb2 / 4; ++w) c[w] = 0u;
+    }
+    sf[sf_offset(r, kb, sel3(g, a.geom.kp[0], a.geom.kp[1], a.geom.kp[2]) >> 7)] = 0;
   }
 }
 
@@ -556,7 +598,6 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   const int stages = d.stages, groups = d.groups, group_warps = d.group_warps, nbox = d.nbox;
   const int dbg = MM_RQ_EXPERIMENTS ? d.dbg : 0;
   const int64_t rows = a.rows;
-  const int kp0 = a.geom.kp[0], kp1 = a.geom.kp[1];
   const int fm1 = a.geom.fmt[1], fm2 = a.geom.fmt[2];
   // Gather table: u16 slot byte offsets, two per word, [block][16 words]: the lane
   // holding half h of block b reads words 16 b + 8 h .. + 7 with two 128-bit loads
@@ -567,8 +608,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
     // Table layouts are swizzled per lane so that the warp-wide 128-bit table loads of
     // the gather are bank-conflict free: lane l of a chunk reads its vector q at
-    // "rotated" slot (q + rot(l)) of its own group (see seg_chunks).
-    const int off1 = a.geom.off[1], off2 = a.geom.off[2];
+    // "rotated" slot (q + rot(l)) of its own group (see tile_chunks).
     const uint32_t sz = (uint32_t)sizeof(ST);
     // slot of channel p: the layout moves 4-channel chunks inside each 32-channel line
     auto slot = [layout](uint32_t p) -> uint32_t {
@@ -579,8 +619,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       for (int t = ct; t < K / 32; t += cn) lay_s[t] = __ldg(layout + t);
     if (tab == 3) {   // in place, one 16-position group per thread: perm[j] -> slot byte offset
       for (int t = ct; t < K / 16; t += cn) {
-        const int j0 = 16 * t, segoff = j0 < off1 ? 0 : (j0 < off2 ? off1 : off2);
-        const int r = ((t - segoff / 16) >> 1) & 3;
+        const int r = (t >> 1) & 3;
         uint4* g = reinterpret_cast<uint4*>(gidx) + 4 * t;
         uint4 w[4];
 #pragma unroll
@@ -593,8 +632,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       }
     } else {          // u16 pairs, one 16-position group (8 words) per thread
       for (int t = ct; t < K / 16; t += cn) {
-        const int j0 = 16 * t, segoff = j0 < off1 ? 0 : (j0 < off2 ? off1 : off2);
-        const int r = ((t - segoff / 16) >> 2) & 1;
+        const int r = (t >> 2) & 1;
         uint4 pv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -625,16 +663,12 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     ptx::named_bar_sync(15, cn);
   }
   const double eps = a.eps;
-  // Work is split into chunks of 16 consecutive blocks of ONE segment (a warp's
-  // lanes never mix segments, so the encode path is warp-uniform); the two lanes of
-  // a pair share a block, 16 channels each.  Warp gw of a group owns the chunks
-  // ch = gw (mod group_warps) of the concatenated chunk list of the three segments
-  // -- the same chunks in every tile, so their first local index per segment is
-  // fixed per warp.
-  const int nch0 = (kp0 / 32 + 15) / 16, nch1 = (kp1 / 32 + 15) / 16;
-  const int cf0 = gw, cf1 = ((gw - nch0) % group_warps + group_warps) % group_warps,
-            cf2 = ((gw - nch0 - nch1) % group_warps + group_warps) % group_warps;
+  // Work is split into chunks of 16 consecutive 32-channel blocks of the reordered
+  // row (tile_chunks; the two lanes of a pair share a block, 16 channels each).  Warp
+  // gw of a group owns the chunks ch = gw (mod group_warps), the same in every tile;
+  // its last warp also zeroes the storage padding blocks (tile_padding).
   const bool e3m2 = fm1 == F_E3M2, e4m3 = fm2 == F_E4M3;
+  const bool has_pad = a.geom.kp[0] != a.geom.n[0] || a.geom.kp[1] != a.geom.n[1] || a.geom.kp[2] != a.geom.n[2];
   int s = grp;           // ring slot and phase of tile i, advanced incrementally
   uint32_t ph = 0;       // (groups < stages: at most one wrap per step)
   for (int64_t i = grp; i < my_tiles; i += groups) {
@@ -758,11 +792,8 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       const int64_t left = rows - r0;
       const int nvalid = left >= R ? R : (left > 0 ? (int)left : 0);
       const ChunkCtx<R> cx{st, smem, gidx, gamma_r, (int)r0, nvalid, group_warps, lane, dbg, tab};
-      seg_chunks<R, NORM, 0, F_E2M1>(a, cx, cf0, rn);
-      if (e3m2) seg_chunks<R, NORM, 1, F_E3M2>(a, cx, cf1, rn);
-      else seg_chunks<R, NORM, 1, F_E2M3>(a, cx, cf1, rn);
-      if (e4m3) seg_chunks<R, NORM, 2, F_E4M3>(a, cx, cf2, rn);
-      else seg_chunks<R, NORM, 2, F_E5M2>(a, cx, cf2, rn);
+      tile_chunks<R, NORM>(a, cx, gw, e3m2, e4m3, rn);
+      if (gw == group_warps - 1 && has_pad && !(dbg & 16)) tile_padding<R>(a, (int)r0, nvalid, lane);
       if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][3 + 2 * i] = ptx::globaltimer_ns();
       if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && gw == 0 && lane == 0) g_rq_trace[blockIdx.x][15] = ptx::globaltimer_ns();
       // ---- release the stage (every warp of the group arrives once) ----
@@ -825,7 +856,7 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   // works on one tile, warp gw of it on chunks gw, gw + group_warps, ... .  Per-tile
   // overhead (ring wait, transpose barrier, row bases) is paid per warp, so each warp
   // should own several chunks (~5 measured best); more groups need more stages.
-  const int nch = (a.geom.kp[0] / 32 + 15) / 16 + (a.geom.kp[1] / 32 + 15) / 16 + (a.geom.kp[2] / 32 + 15) / 16;
+  const int nch = (a.K / 32 + 15) / 16;   // chunks per tile (tile_chunks)
   const int W = rq_max_threads(R, NORM) / 32 - 1;
   int gw = (nch + 4) / 5;
   if (gw < 1) gw = 1;
