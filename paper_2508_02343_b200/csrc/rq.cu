@@ -841,6 +841,7 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   static const int tab32 = [] { const char* e = getenv("MM_RQ_TAB32"); return e ? atoi(e) : 0; }();
   if (tab32 && a.K % 4 == 0 && (budget - (size_t)a.K * 4) / stage_bytes >= 3) d.perm_smem = 3;
   else d.perm_smem = (budget - tab_need) / stage_bytes >= 3 ? 1 : ((budget - gtab) / stage_bytes >= 2 ? 2 : 0);
+  { const char* e = getenv("MM_RQ_TABMODE"); if (e && atoi(e) >= 0 && atoi(e) <= 3) d.perm_smem = atoi(e); }   // tuning
   if (d.perm_smem != 3 && (size_t)a.K * 2 * R > 65536) d.perm_smem = 0;   // u16 table holds byte offsets
   size_t tab_bytes = d.perm_smem == 3 ? (size_t)a.K * 4 : (d.perm_smem == 1 ? tab_need : (d.perm_smem == 2 ? gtab : 0));
   // gather layout (R = 2 with a table only): per-line words for the transpose
@@ -862,8 +863,16 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   if (gw < 1) gw = 1;
   if (gw > W) gw = W;
   int groups = W / gw;
-  if (groups > stages - 1) {   // stage-limited: fewer, larger groups that still use every warp
-    groups = stages - 1;
+  // Ring lookahead: each group holds its stage while it works on the tile, so only
+  // stages - groups tiles can be in flight from HBM ahead of the groups.
+  // Two tiles of lookahead where the ring is deep (K = 4096, 12 stages: 10 groups instead
+  // of 11, 16384 x 4096 41.2 -> 39.0 us); one where stages are scarce (K = 14336: 3
+  // stages, 2 groups -- one group of 23 warps is 28 % slower).  MM_RQ_LOOKAHEAD: tuning.
+  static const int look_env = [] { const char* e = getenv("MM_RQ_LOOKAHEAD"); return e ? atoi(e) : 0; }();
+  const int look = look_env >= 1 ? look_env : (stages >= 8 ? 2 : 1);
+  const int max_groups = stages - look > 1 ? stages - look : 1;
+  if (groups > max_groups) {   // stage-limited: fewer, larger groups that still use every warp
+    groups = max_groups;
     gw = W / groups;
     if (gw > nch) gw = nch;
   }
@@ -877,7 +886,8 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
     if (gw > nch) gw = nch;
   }
   { const char* e = getenv("MM_RQ_GW"); if (e && atoi(e) >= 1 && atoi(e) <= W) { gw = atoi(e); groups = W / gw; } }   // tuning
-  if (groups > stages - 1) groups = stages - 1;
+  { const char* e = getenv("MM_RQ_GROUPS"); if (e && atoi(e) >= 1 && atoi(e) <= W) { groups = atoi(e); gw = W / groups; if (gw > nch) gw = nch; } }
+  if (groups > max_groups) groups = max_groups;
   if (groups < 1) groups = 1;
   d.group_warps = gw;
   d.groups = groups;
