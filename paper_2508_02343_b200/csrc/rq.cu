@@ -341,6 +341,23 @@ __device__ __forceinline__ void quantize_rows(const typename Slot<R>::T (&v)[NV]
   }
 }
 
+// Shared-memory loads by 32-bit shared address: with a warp-uniform base the gather
+// becomes one LDS [R + UR] per slot (no generic-to-shared window arithmetic per load).
+__device__ __forceinline__ void lds_slot(uint32_t a, uint16_t& v) {
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+}
+__device__ __forceinline__ void lds_slot(uint32_t a, uint32_t& v) {
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+}
+__device__ __forceinline__ void lds_slot(uint32_t a, uint2& v) {
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
 // Per-tile context of a consumer warp (everything tile_chunks needs besides the plan).
 template <int R> struct ChunkCtx {
   const uint8_t* st;        // stage: 256-channel boxes of row-interleaved slots
@@ -377,6 +394,15 @@ __device__ __forceinline__ void tile_chunks(const RqArgs& a, const ChunkCtx<R>& 
   const unsigned r0 = (unsigned)cx.r0;
   const uint32_t st_off = __reduce_max_sync(0xffffffffu, (uint32_t)(cx.st - cx.smem0));
   const uint8_t* const st_u = cx.smem0 + st_off;
+  const uint32_t st_s = __reduce_max_sync(0xffffffffu, ptx::smem_u32(cx.st));   // stage, shared address
+  // u16 table: the lane's two 16-byte table vectors of block b sit at 64 b + 32 h + 16 rot
+  // and 64 b + 32 h + 16 (rot ^ 1) (rot: the table build's per-lane swap)
+  // (opaque moves: keep the two per-lane bases in registers instead of recomputing them
+  // from the thread index in every chunk)
+  const uint32_t trot = (uint32_t)((cx.lane >> 2) & 1);
+  uint32_t tb0, tb1;
+  asm("mov.b32 %0, %1;" : "=r"(tb0) : "r"(ptx::smem_u32(cx.gidx) + 32u * (uint32_t)h + 16u * trot));
+  asm("mov.b32 %0, %1;" : "=r"(tb1) : "r"(ptx::smem_u32(cx.gidx) + 32u * (uint32_t)h + 16u * (trot ^ 1u)));
   // per-tile row bases of the three segments' code rows and scale atoms
   const unsigned sf_row = (r0 & 31) * 16 + ((r0 >> 5) & 3) * 4;
   for (int c = c_first; c < nch; c += cx.group_warps) {
@@ -398,14 +424,12 @@ __device__ __forceinline__ void tile_chunks(const RqArgs& a, const ChunkCtx<R>& 
         v[4 * q4 + 3] = *reinterpret_cast<const ST*>(st_u + e.w);
       }
     } else if (cx.tab) {
-      const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + 16 * bg + 8 * h);
-      const int rot = (cx.lane >> 2) & 1;          // the table build's per-lane swap
-      const uint4 p0 = gp[rot], p1 = gp[rot ^ 1];
+      const uint4 p0 = lds_u4(tb0 + 64u * (uint32_t)bg), p1 = lds_u4(tb1 + 64u * (uint32_t)bg);
       const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        v[2 * q + 0] = *reinterpret_cast<const ST*>(st_u + (pr[q] & 0xFFFFu));
-        v[2 * q + 1] = *reinterpret_cast<const ST*>(st_u + (pr[q] >> 16));
+        lds_slot(st_s + (pr[q] & 0xFFFFu), v[2 * q + 0]);
+        lds_slot(st_s + (pr[q] >> 16), v[2 * q + 1]);
       }
     } else {
       const ST* slots = reinterpret_cast<const ST*>(cx.st);
@@ -529,7 +553,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   // (+ the gather layout's per-line words for the transpose, R = 2 only)
   const size_t tab_core = perm_copy + ((d.perm_smem == 1 || d.perm_smem == 2) ? ((size_t)K * 2 + 15) / 16 * 16 : 0);
   const uint32_t* layout = R == 2 ? a.layout : nullptr;
-  const size_t tab_bytes = tab_core + (layout ? ((size_t)(K / 32) * 4 + 15) / 16 * 16 : 0);
+  const size_t tab_bytes = tab_core + (layout ? (size_t)d.nbox * 32 : 0);
   uint32_t* lay_s = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + tab_core);
   const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
   uint32_t* gidx = d.perm_smem == 3 ? reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes)   // K words
@@ -615,8 +639,8 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       if (!layout) return p;
       return (p & ~31u) | (((__ldg(layout + (p >> 5)) >> (4 * ((p >> 2) & 7))) & 7u) << 2) | (p & 3u);
     };
-    if (layout)
-      for (int t = ct; t < K / 32; t += cn) lay_s[t] = __ldg(layout + t);
+    if (layout)   // one word per 32-channel line of every box; lines past K keep the natural order
+      for (int t = ct; t < 8 * nbox; t += cn) lay_s[t] = t < K / 32 ? __ldg(layout + t) : 0x76543210u;
     if (tab == 3) {   // in place, one 16-position group per thread: perm[j] -> slot byte offset
       for (int t = ct; t < K / 16; t += cn) {
         const int r = (t >> 1) & 3;
@@ -680,6 +704,38 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     // registers, so the norm needs no second pass over the stage.)
     double nhi[4] = {0, 0, 0, 0}, nlo[4] = {0, 0, 0, 0};
     if constexpr (R > 1) {
+      if constexpr (R == 2 && !NORM) {
+        // Lane l owns channels 8 l .. 8 l + 7 of each box, i.e. 16-byte chunks 2 (l & 3) and
+        // 2 (l & 3) + 1 of 32-channel line l / 4.  Lanes 4..7 of every 8 store their odd
+        // chunk first, so the 8 chunks of each store instruction fill 8 different bank
+        // groups (4 wavefronts per 512 B instead of 8): the lane reads its row words as two
+        // 8-byte halves in store order (no register selects), and the chunk positions come
+        // from the plan's parity-preserving gather layout (identity past K, see lay_s).
+        const int f = (lane >> 2) & 1;
+        const int qf = 2 * (lane & 3) + f;               // chunk stored first
+        const uint32_t shf = 4u * (uint32_t)qf, shs = 4u * (uint32_t)(qf ^ 1);
+        for (int b = gw; b < nbox && !(dbg & 2); b += group_warps) {
+          uint8_t* box = st + b * 1024;
+          const uint2 a0 = *reinterpret_cast<const uint2*>(box + lane * 16 + 8 * f);
+          const uint2 a1 = *reinterpret_cast<const uint2*>(box + 512 + lane * 16 + 8 * f);
+          const uint2 b0 = *reinterpret_cast<const uint2*>(box + lane * 16 + 8 * (f ^ 1));
+          const uint2 b1 = *reinterpret_cast<const uint2*>(box + 512 + lane * 16 + 8 * (f ^ 1));
+          __syncwarp();
+          const uint4 cf = make_uint4(__byte_perm(a0.x, a1.x, 0x5410), __byte_perm(a0.x, a1.x, 0x7632),
+                                      __byte_perm(a0.y, a1.y, 0x5410), __byte_perm(a0.y, a1.y, 0x7632));
+          const uint4 cs = make_uint4(__byte_perm(b0.x, b1.x, 0x5410), __byte_perm(b0.x, b1.x, 0x7632),
+                                      __byte_perm(b0.y, b1.y, 0x5410), __byte_perm(b0.y, b1.y, 0x7632));
+          uint32_t pf = (uint32_t)qf, ps = (uint32_t)(qf ^ 1);
+          if (layout) {
+            const uint32_t lw = lay_s[8 * b + (lane >> 2)];
+            pf = (lw >> shf) & 7u;
+            ps = (lw >> shs) & 7u;
+          }
+          uint4* line = reinterpret_cast<uint4*>(box + (lane >> 2) * 128);
+          line[pf] = cf;
+          line[ps] = cs;
+        }
+      } else
       for (int b = gw; b < nbox && !(dbg & 2); b += group_warps) {
         uint8_t* box = st + b * 512 * R;
         uint4 w[R];
@@ -847,7 +903,7 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   // gather layout (R = 2 with a table only): per-line words for the transpose
   static const int no_layout = [] { const char* e = getenv("MM_RQ_NO_LAYOUT"); return e ? atoi(e) : 0; }();  // A/B
   if (R != 2 || d.perm_smem == 0 || no_layout) d.a.layout = nullptr;
-  if (d.a.layout) tab_bytes += ((size_t)(a.K / 32) * 4 + 15) / 16 * 16;
+  if (d.a.layout) tab_bytes += (size_t)d.nbox * 32;   // one word per 32-channel line of every box
   int stages = (int)((budget - tab_bytes) / stage_bytes);
   if (stages > 32) stages = 32;
   { const char* e = getenv("MM_RQ_STAGES"); if (e && atoi(e) >= 2 && atoi(e) < stages) stages = atoi(e); }
