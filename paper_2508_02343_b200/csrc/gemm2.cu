@@ -25,6 +25,8 @@
 #include <map>
 #include <mutex>
 #include <utility>
+#include <vector>
+#include <algorithm>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -33,6 +35,7 @@ namespace mmx {
 namespace {
 
 constexpr int kThreads2 = 256;
+constexpr int kMaxPairs = 80;   // >= SMs / 2 (148 SMs on B200)
 // Timeline trace (env MM_GEMM_DEBUG & 32; read with mm_debug_gemm_trace): per CTA
 // [start, setup, first stage ready, tile0 start, tile0 issued, tile1 start, tile1
 // issued, tile2 start, tile2 issued, epi0 ready, epi1 ready, epi2 ready, epi done].
@@ -83,6 +86,8 @@ struct Gemm2Dev {
   uint16_t* y_mc;        // NVLS: multicast view of all ranks' Y (nullptr: TMA stores)
   int64_t mc_col_off;    // this rank's column offset in the full Y
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
+  int sched2;  // 1: two-wave item table (build_split2): every pair one whole tile + at most one narrow item
+  uint32_t item[2 * kMaxPairs];   // [pair][2]: bit 31 valid | mb2 | (n0 / 64) << 10 | (w / 64) << 24
 };
 
 // Tile raster: groups of up to 8 pair-row blocks (2048 rows of A) sweep all of N
@@ -106,6 +111,7 @@ __device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int ra
 // order, so every pair writes its partial head first and the finisher of that
 // tile -- the next pair, at the end of its own range -- finds it ready.
 __device__ __forceinline__ int num_items(const Gemm2Dev& p, int pair, int npairs, int S) {
+  if (p.sched2) return (int)(p.item[2 * pair] >> 31) + (int)(p.item[2 * pair + 1] >> 31);
   if (!p.stream_k) return (p.num_tiles - pair + npairs - 1) / npairs;
   const int64_t W = (int64_t)p.num_tiles * S;
   const int64_t lo = pair * W / npairs, hi = (pair + 1) * W / npairs;
@@ -120,6 +126,24 @@ __device__ __forceinline__ void work_item(const Gemm2Dev& p, int pair, int npair
   const int64_t base = (int64_t)t * S;
   s0 = (int)(lo > base ? lo - base : 0);
   s1 = (int)(hi - base < S ? hi - base : S);
+}
+
+// Output block of item i of a pair: rows [256 mb2, +256), columns [n0, n0 + w).  Whole
+// tiles (w = 256) in the data-parallel / stream-K schedules; in the two-wave schedule
+// (p.sched2) a pair's second item may be 64 / 128 / 192 columns wide and start 64 rows
+// into a W scale atom (its MMAs then read SFB two TMEM words in; see build_split2).
+__device__ __forceinline__ void item_coords(const Gemm2Dev& p, int pair, int i, int t, int& mb2, int& n0, int& w) {
+  if (p.sched2) {
+    const uint32_t e = p.item[2 * pair + i];
+    mb2 = (int)(e & 1023u);
+    n0 = (int)((e >> 10) & 4095u) * 64;
+    w = (int)((e >> 24) & 7u) * 64;
+    return;
+  }
+  int nb;
+  tile_coords(t, p.num_m2, p.num_n, p.raster, mb2, nb);
+  n0 = nb * 256;
+  w = 256;
 }
 
 template <int G>
@@ -229,7 +253,6 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   ptx::grid_dep_wait();   // A, W, scales may come from the preceding kernel; Y may still be read by it
   if (trace && warp == 1) { g_trace[blockIdx.x][0] = t_start; g_trace[blockIdx.x][1] = ptx::globaltimer_ns(); }
   const int64_t M = p.M, N = p.N;
-  const int num_m2 = p.num_m2;
   const int S = p.nst0 + p.nst1 + p.nst2;
   const int n_items = num_items(p, pair, npairs, S);
 
@@ -247,11 +270,12 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       for (int it = 0; it < n_items; ++it) {
         int t, s0, s1;
         work_item(p, pair, npairs, S, it, t, s0, s1);
-        int mb2, nb;
-        tile_coords(t, num_m2, p.num_n, p.raster, mb2, nb);
+        int mb2, nt0, w;
+        item_coords(p, pair, it, t, mb2, nt0, w);
         const int m0 = mb2 * 256 + 128 * (int)rank;      // this CTA's A rows
-        const int n0 = nb * 256 + 128 * (int)rank;       // this CTA's W rows (its half of N)
+        const int n0 = nt0 + (w / 2) * (int)rank;        // this CTA's W rows (its half of the item's N)
         const int mgrp = mb2 * 2 + (int)rank;           // 128-row scale group of A
+        const int rgb = nt0 >> 7;                       // first 128-row scale group of W
 #pragma unroll
         for (int g = 0; g < 3; ++g) {
           const int nst = g == 0 ? p.nst0 : (g == 1 ? p.nst1 : p.nst2);
@@ -289,7 +313,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
 #pragma unroll
               for (int rg = 0; rg < 2; ++rg)
                 ptx::tma_load_2d_cg2(ptx::smem_u32(sSFB + stage * SFB_BYTES + rg * 1024), tsb, fb, 0,
-                                     (nb * 2 + rg) * kp128 + atom0);
+                                     (rgb + rg) * kp128 + atom0);
             }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
@@ -315,6 +339,12 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         work_item(p, pair, npairs, S, it, t, s0, s1);
         const int acc = it & 1;
         const uint32_t d_t = tmem_base + (acc ? ACC1_COL : 0);
+        int mb2_, nt0, w;
+        item_coords(p, pair, it, t, mb2_, nt0, w);
+        // the item's N in the instruction descriptor (bits 17-22: N >> 3); an item that
+        // starts 64 rows into a W scale atom reads SFB two TMEM words in
+        const uint32_t nfield = ~(0x3Fu << 17), nbits = (uint32_t)(w >> 3) << 17;
+        const uint32_t sfb_off = (nt0 & 127) ? 2u : 0u;
         ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), ((it >> 1) & 1) ^ 1, 22, it, t);   // tile it-2 drained acc
         if (trace && it == 1) g_trace[blockIdx.x][16] = ptx::globaltimer_ns();
         if (it > 0) ptx::mbar_wait(ptx::smem_u32(&tovl[acc ^ 1]), ((it - 1) >> 1) & 1, 25, it, t);  // overlap of it-1
@@ -327,7 +357,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         for (int g = 0; g < 3; ++g) {
           const int nst = g == 0 ? p.nst0 : (g == 1 ? p.nst1 : p.nst2);
           const int n_g = g == 0 ? p.n0 : (g == 1 ? p.n1 : p.n2);
-          const uint32_t idesc = g == 0 ? p.idesc0 : (g == 1 ? p.idesc1 : p.idesc2);
+          const uint32_t idesc = ((g == 0 ? p.idesc0 : (g == 1 ? p.idesc1 : p.idesc2)) & nfield) | nbits;
           const int kstage = g == 0 ? 256 : 128;                    // K per stage
           const int kmma = g == 0 ? 64 : 32;                        // K per MMA
           const int sbase = g == 0 ? 0 : (g == 1 ? p.nst0 : p.nst0 + p.nst1);
@@ -345,9 +375,10 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
             const uint64_t sdb0 = ptx::smem_desc(sSFB0 + stage * SFB_BYTES, 0, 128, 0);
             const uint64_t sdb1 = ptx::smem_desc(sSFB0 + stage * SFB_BYTES + 1024, 0, 128, 0);
             if (nmma == 4 && !no_mma) {
-              if (g == 0) ptx::stage_f4_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage);
+              if (g == 0) ptx::stage_f4_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage,
+                                            sfb_t + sfb_off);
               else ptx::stage_f8f6_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage,
-                                       (p.dbg & 64) ? 0u : 1u);
+                                       (p.dbg & 64) ? 0u : 1u, sfb_t + sfb_off);
               accum = 1;
             } else {
               // partial stage: scale copies for the atoms it uses, then nmma MMAs
@@ -362,10 +393,10 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
                   if (g == 0) {
                     const uint32_t sid = 2u * (k & 1);
                     ptx::tc_mma_mxf4_cg2(d_t, ad + 2 * k, bd + 2 * k, idesc | (sid << 29) | (sid << 4),
-                                         sfa_t + 4 * (k >> 1), sfb_t + (k >> 1) * 8, accum);
+                                         sfa_t + 4 * (k >> 1), sfb_t + sfb_off + (k >> 1) * 8, accum);
                   } else {
                     ptx::tc_mma_mxf8f6f4_cg2(d_t, ad + 2 * k, bd + 2 * k, idesc | ((uint32_t)k << 29) | ((uint32_t)k << 4),
-                                             sfa_t, sfb_t, accum);
+                                             sfa_t, sfb_t + sfb_off, accum);
                   }
                   accum = 1;
                 }
@@ -399,8 +430,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     for (int it = 0; it < n_items; ++it) {
       int t, s0, s1;
       work_item(p, pair, npairs, S, it, t, s0, s1);
-      int mb2, nb;
-      tile_coords(t, num_m2, p.num_n, p.raster, mb2, nb);
+      int mb2, n0, w;
+      item_coords(p, pair, it, t, mb2, n0, w);
+      const int nch = w / 32;   // 32-column chunks of this item (8 for a whole tile)
       // stream-K roles of this item: leave a partial (head of a tile) / add one (tail)
       const bool to_ws = s1 < S, from_ws = s0 > 0;
       const int wrow = 128 * (int)rank + q * 32 + lane;   // row inside the 256-row pair tile
@@ -448,7 +480,6 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       if (trace && q == 0 && it == 0 && rank == 0) g_trace[blockIdx.x][21] = clock64();
       ptx::tc_fence_after();
       const int row0 = mb2 * 256 + 128 * (int)rank + q * 32;
-      const int n0 = nb * 256;
       const uint32_t acc_col = acc ? ACC1_COL : 0;
       uint32_t rn[32];   // chunk 1 of the drain order, loaded together with chunk 0
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc_col;
@@ -462,26 +493,29 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(hgo));
         if (lane == 0) ptx::bulk_wait_group_read<0>();   // this warp's earlier stores have read `stg`
         __syncwarp();
-        drain_chunks<NP>(tys, p.ndst, trow, sA + (4 + q) * 8192, 0, 4, n0, row0, lane);
+        drain_chunks<NP>(tys, p.ndst, trow, sA + (4 + q) * 8192, 0, min(4, nch), n0, row0, lane);
         continue;
       }
+      // acc0 of a whole tile: its overlap with acc1 (columns 208..255) lives in chunks 6,
+      // 7 -> drain those first (a narrower item does not reach the overlap); acc1: its
+      // overlap is its own columns 0..47 -> chunks 0, 1 come first anyway.  The first two
+      // chunks are loaded back to back and the overlap released before any conversion,
+      // so the next tile's MMAs wait for two TMEM loads only.
+      const int rot = (acc == 0 && nch == 8) ? 6 : 0;
 #pragma unroll 1
-      for (int i = 0; i < 8; ++i) {
-        // acc0: its overlap (columns 208..255) lives in chunks 6, 7 -> drain those first;
-        // acc1: its overlap is its own columns 0..47 -> chunks 0, 1 come first anyway.
-        // The two overlap chunks are loaded back to back and released before any
-        // conversion, so the next tile's MMAs wait for two TMEM loads only.
-        const int c = acc ? i : (i + 6) & 7;
+      for (int i = 0; i < nch; ++i) {
+        const int c = (i + rot) & 7;
         uint32_t r[32];
         if (i == 0) {
           if (trace && q == 0 && it == 0 && rank == 0) g_trace[blockIdx.x][19] = clock64();
           ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
-          ptx::tmem_ld_32x32b_x32(trow + 32 * (acc ? 1 : 7), rn);
+          ptx::tmem_ld_32x32b_x32(trow + 32 * ((1 + rot) & 7), rn);
           ptx::tc_wait_ld();
           if (trace && q == 0 && it == 0 && rank == 0) g_trace[blockIdx.x][20] = clock64();
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_cluster(tovl_leader + 8 * acc);   // overlap drained
+          if (nch == 2 && lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);   // all drained
           if (trace && q == 0 && it == 0) g_trace[blockIdx.x][17 + (int)rank] = ptx::globaltimer_ns();
         } else if (i == 1) {
 #pragma unroll
@@ -489,7 +523,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         } else {
           ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
           ptx::tc_wait_ld();
-          if (i == 7) {   // whole accumulator drained
+          if (i == nch - 1) {   // whole accumulator drained
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
@@ -580,8 +614,8 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     const int it = n_items - 1;
     int t, s0, s1;
     work_item(p, pair, npairs, S, it, t, s0, s1);
-    int mb2, nb;
-    tile_coords(t, num_m2, p.num_n, p.raster, mb2, nb);
+    int mb2, n0, w;
+    item_coords(p, pair, it, t, mb2, n0, w);
     const int acc = it & 1;
     // single phase: the epilogue warps saw tfull.  A suspended wait: warps 1 (odd CTA)
     // and 2 have no role and would otherwise spin for the whole kernel, stealing issue
@@ -590,7 +624,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     ptx::tc_fence_after();
     const int q = warp & 3;
     const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + (acc ? ACC1_COL : 0);
-    drain_chunks<NP>(tys, p.ndst, trow, sA + q * 8192, 4, 8, nb * 256, mb2 * 256 + 128 * (int)rank + q * 32, lane);
+    drain_chunks<NP>(tys, p.ndst, trow, sA + q * 8192, 4, w / 32, n0, mb2 * 256 + 128 * (int)rank + q * 32, lane);
     if (lane == 0) {
       if constexpr (NP == 1) ptx::bulk_wait_group_read<0>();
       else ptx::bulk_wait_group<0>();
@@ -637,6 +671,50 @@ bool use_stream_k(const GemmArgs& a, const GemmConfig& cfg) {
   const int npairs = pair_grid(a, cfg) / 2;
   return sk_env_on && !cfg.no_stream_k && !cfg.no_workspace && a.n_dst == 0 && npairs > 0 &&
          num_tiles > npairs && num_tiles % npairs != 0 && num_tiles < 4 * npairs;
+}
+
+// Two-wave schedule for a ragged second wave (P pairs < T tiles < 2 P, e.g. q_proj: 128
+// tiles on 74 pairs).  Every pair takes ONE whole 256 x 256 tile; what is left of each
+// 256-row block (its columns past the whole tiles) is cut into narrow items of wn 64-column
+// units (wn <= 3: 192 columns, so an item that starts 64 rows into a W scale atom still
+// spans two row groups), at most one per pair.  The whole tiles per row block a_b are
+// chosen by a small DP so that the leftover splits into few items: q_proj ends with 6 row
+// blocks of 10 tiles + 8 items and 2 of 7 tiles + 12 items = 74 tiles + 72 items of 192
+// columns, i.e. no pair computes more than 448 columns instead of two 256-column tiles.
+// A narrow item still reads the whole 128-row A slab per stage, so it costs more than its
+// share of columns; the schedule is used only when it balances the work (see run2).
+bool build_split2(int num_m2, int64_t N, int P, uint32_t* item) {
+  const int U = (int)((N + 63) / 64);   // 64-column units per row block
+  const int A = U / 4;                  // whole tiles per row block
+  if (P < 1 || P > kMaxPairs || (int64_t)num_m2 * A < P || (int64_t)num_m2 * U <= 4LL * P || num_m2 > 64) return false;
+  for (int wn = 1; wn <= 3; ++wn) {
+    // dp[b + 1][s]: fewest items over row blocks 0..b using s whole tiles; choice[b][s] = a_b
+    const int INF = 1 << 29;
+    std::vector<std::vector<int>> dp(num_m2 + 1, std::vector<int>(P + 1, INF)), ch(num_m2, std::vector<int>(P + 1, -1));
+    dp[0][0] = 0;
+    for (int b = 0; b < num_m2; ++b)
+      for (int s0 = 0; s0 <= P; ++s0) {
+        if (dp[b][s0] >= INF) continue;
+        for (int a = 0; a <= A && s0 + a <= P; ++a) {
+          const int v = dp[b][s0] + (U - 4 * a + wn - 1) / wn;
+          if (v < dp[b + 1][s0 + a]) { dp[b + 1][s0 + a] = v; ch[b][s0 + a] = a; }
+        }
+      }
+    if (dp[num_m2][P] > P) continue;
+    std::vector<int> a_b(num_m2);
+    for (int b = num_m2 - 1, s1 = P; b >= 0; --b) { a_b[b] = ch[b][s1]; s1 -= a_b[b]; }
+    std::vector<uint32_t> full, narrow;
+    for (int b = 0; b < num_m2; ++b) {
+      for (int k = 0; k < a_b[b]; ++k) full.push_back((uint32_t)b | (uint32_t)(4 * k) << 10 | 4u << 24);
+      for (int u = 4 * a_b[b]; u < U; u += wn) narrow.push_back((uint32_t)b | (uint32_t)u << 10 | (uint32_t)std::min(wn, U - u) << 24);
+    }
+    for (int q = 0; q < P; ++q) {
+      item[2 * q] = full[q] | 0x80000000u;
+      item[2 * q + 1] = q < (int)narrow.size() ? (narrow[q] | 0x80000000u) : 0u;
+    }
+    return true;
+  }
+  return false;
 }
 
 template <int STAGES, int NP>
@@ -703,6 +781,13 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   const int grid = pair_grid(a, cfg);
   const int npairs = grid / 2;
   p.stream_k = use_stream_k(a, cfg) ? 1 : 0;
+  {
+    // two-wave schedule (build_split2) for a ragged second wave; MM_GEMM_SPLIT2=0/1 forces it
+    const char* e = getenv("MM_GEMM_SPLIT2");
+    const bool want = e ? atoi(e) == 1 : true;
+    p.sched2 = (!p.stream_k && want && p.num_tiles > npairs && p.num_tiles < 2 * npairs &&
+                build_split2(p.num_m2, a.N, npairs, p.item)) ? 1 : 0;
+  }
   // Helper drain of the last tile: for few tiles per pair (<= 4), where the exposed final
   // drain is a visible share of the kernel (q_proj: 27 -> 25 us); measured ~1 % slower
   // with ~14 tiles per pair (70B down_proj), so off there.  MM_GEMM_HELPERS=0/1 forces it.

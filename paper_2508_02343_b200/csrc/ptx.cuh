@@ -296,7 +296,10 @@ __device__ __forceinline__ void tc_mma_mxf4_cg2(uint32_t d, uint64_t adesc, uint
 __device__ __forceinline__ void stage_f8f6_cg2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id0, uint32_t sfa,
                                                uint32_t sfb, uint64_t sda, uint64_t sdb0, uint64_t sdb1,
                                                uint32_t accum, uint32_t empty_bar, uint32_t do_cp = 1,
-                                               uint16_t mask = 3) {
+                                               uint32_t sfbm = 0xFFFFFFFFu, uint16_t mask = 3) {
+  // sfbm: the SFB address the MMAs read (default sfb).  An item whose first output
+  // column sits 64 rows into a scale atom reads from sfb + 2 (two 32-row TMEM words).
+  if (sfbm == 0xFFFFFFFFu) sfbm = sfb;
   const uint32_t sfb4 = sfb + 4;
   const uint32_t id1 = id0 | (1u << 29) | (1u << 4), id2 = id0 | (2u << 29) | (2u << 4), id3 = id0 | (3u << 29) | (3u << 4);
   asm volatile(
@@ -310,22 +313,25 @@ __device__ __forceinline__ void stage_f8f6_cg2(uint32_t d, uint64_t ad, uint64_t
       "@c tcgen05.cp.cta_group::2.32x128b.warpx4 [%4], %6;\n\t"
       "@c tcgen05.cp.cta_group::2.32x128b.warpx4 [%5], %7;\n\t"
       "@c tcgen05.cp.cta_group::2.32x128b.warpx4 [%13], %8;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%5], acc;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a1, b1, %10, [%4], [%5], one;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a2, b2, %11, [%4], [%5], one;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a3, b3, %12, [%4], [%5], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%17], acc;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a1, b1, %10, [%4], [%17], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a2, b2, %11, [%4], [%17], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], a3, b3, %12, [%4], [%17], one;\n\t"
       "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%14], %15;\n\t}"
       ::"r"(d), "l"(ad), "l"(bd), "r"(id0), "r"(sfa), "r"(sfb), "l"(sda), "l"(sdb0), "l"(sdb1), "r"(accum),
-        "r"(id1), "r"(id2), "r"(id3), "r"(sfb4), "r"(empty_bar), "h"(mask), "r"(do_cp)
+        "r"(id1), "r"(id2), "r"(id3), "r"(sfb4), "r"(empty_bar), "h"(mask), "r"(do_cp), "r"(sfbm)
       : "memory");
 }
 // One full FP4 stage: 2 atoms each of SFA and of SFB row groups 0/1 + 4
 // kind::mxf4 MMAs (K = 64; MMA k uses atom k/2, scale-factor ids 0/2) + commit.
 __device__ __forceinline__ void stage_f4_cg2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id0, uint32_t sfa,
                                              uint32_t sfb, uint64_t sda, uint64_t sdb0, uint64_t sdb1,
-                                             uint32_t accum, uint32_t empty_bar, uint16_t mask = 3) {
-  // SFA atoms at columns sfa, sfa+4; SFB (atom a, row group r) at sfb + (2a + r) * 4
-  const uint32_t sfa4 = sfa + 4, sfb4 = sfb + 4, sfb8 = sfb + 8, sfb12 = sfb + 12;
+                                             uint32_t accum, uint32_t empty_bar, uint32_t sfbm = 0xFFFFFFFFu,
+                                             uint16_t mask = 3) {
+  // SFA atoms at columns sfa, sfa+4; SFB (atom a, row group r) at sfb + (2a + r) * 4;
+  // the MMAs read SFB from sfbm (default sfb; +2 for an item starting 64 rows into an atom)
+  if (sfbm == 0xFFFFFFFFu) sfbm = sfb;
+  const uint32_t sfa4 = sfa + 4, sfb4 = sfb + 4, sfb8 = sfb + 8, sfb12 = sfb + 12, sfbm8 = sfbm + 8;
   const uint32_t id2 = id0 | (2u << 29) | (2u << 4);
   asm volatile(
       "{\n\t.reg .pred p, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3, sa1, s01, s11;\n\t"
@@ -341,13 +347,13 @@ __device__ __forceinline__ void stage_f4_cg2(uint32_t d, uint64_t ad, uint64_t b
       "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%12], %8;\n\t"
       "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%13], s01;\n\t"
       "@p tcgen05.cp.cta_group::2.32x128b.warpx4 [%14], s11;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], acc;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a1, b1, %10, [%4], [%5], one;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a2, b2, %3, [%11], [%13], one;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a3, b3, %10, [%11], [%13], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%17], acc;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a1, b1, %10, [%4], [%17], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a2, b2, %3, [%11], [%18], one;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], a3, b3, %10, [%11], [%18], one;\n\t"
       "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%15], %16;\n\t}"
       ::"r"(d), "l"(ad), "l"(bd), "r"(id0), "r"(sfa), "r"(sfb), "l"(sda), "l"(sdb0), "l"(sdb1), "r"(accum),
-        "r"(id2), "r"(sfa4), "r"(sfb4), "r"(sfb8), "r"(sfb12), "r"(empty_bar), "h"(mask)
+        "r"(id2), "r"(sfa4), "r"(sfb4), "r"(sfb8), "r"(sfb12), "r"(empty_bar), "h"(mask), "r"(sfbm), "r"(sfbm8)
       : "memory");
 }
 __device__ __forceinline__ void commit_cg2_mc_elect(uint32_t bar, uint16_t mask = 3) {
