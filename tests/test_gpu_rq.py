@@ -72,7 +72,8 @@ def test_format_variants_and_rules(fmt6, fmt8, rule):
 
 @pytest.mark.parametrize("K", [4096, 14336, 28672])
 def test_llama_widths_calibrated(K):
-    """The three tile widths (R = 4 / 2 / 1 rows per tile) on calibrated plans."""
+    """Calibrated plans at the Llama widths (two-row tiles up to K = 16384, one-row beyond;
+    four-row tiles: test_forced_tile_rows)."""
     cal_x = gen_act(1024, K, 1000, 2000)
     plan = mm.mm_calibrate_thresholds(cal_x.cuda())
     rows = 2048 if K == 4096 else 256
@@ -200,3 +201,24 @@ def test_gather_layout_does_not_change_results(K, n):
         if n[g]:
             assert torch.equal(a0.codes2d(g), a1.codes2d(g)), g
     _parity(x, p_lay)
+
+
+@pytest.mark.parametrize("rows", [1, 4])
+def test_forced_tile_rows(rows):
+    """The one- and four-row tile variants of the RQ kernel (the automatic dispatch
+    uses two-row tiles up to K = 16384): the parity tests above re-run in a child
+    process with MM_RQ_ROWS forcing R (the library reads it once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MM_RQ_ROWS=str(rows))
+    sel = "cfg1 or ragged_rows or segment_shapes or format_variants or rmsnorm_fused or strided"
+    if rows == 1:
+        sel += " or widths"
+    else:   # four-row tiles of K >= 14336 do not fit shared memory (the dispatch never picks them)
+        sel = f"({sel}) and not 14336"
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_rq.py"), "-k", sel],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
