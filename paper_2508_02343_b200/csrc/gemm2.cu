@@ -52,6 +52,11 @@ constexpr int SF_STRIDE = 24;            // TMEM columns per scale slot: SFA 2x4
 // early, so the next tile's MMAs (into the other accumulator) start after ~1/4 of
 // the epilogue instead of after all of it.
 constexpr int ACC1_COL = 208;
+// An item of <= 208 columns in the odd accumulator sits at column 256 instead: it does not
+// overlap the even accumulator at all, so its MMAs need not wait for the previous item's
+// overlap columns to drain (that wait idles the tensor pipe for the previous item's MMA
+// completion + first TMEM loads, ~1 us between the two items of the two-wave schedule).
+__host__ __device__ constexpr uint32_t acc_col(int acc, int w) { return acc == 0 ? 0u : (w <= 208 ? 256u : (uint32_t)ACC1_COL); }
 constexpr int SF_COL = 464;
 // epilogue staging: 4 warps x NB buffers x (32 x 32 BF16); one buffer per warp when
 // 6 operand stages take the shared memory
@@ -338,16 +343,24 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         int t, s0, s1;
         work_item(p, pair, npairs, S, it, t, s0, s1);
         const int acc = it & 1;
-        const uint32_t d_t = tmem_base + (acc ? ACC1_COL : 0);
         int mb2_, nt0, w;
         item_coords(p, pair, it, t, mb2_, nt0, w);
+        const uint32_t d_t = tmem_base + acc_col(acc, w);
+        bool ovl = false;   // does this item's accumulator overlap the previous item's?
+        if (it > 0) {
+          int tp, s0p, s1p, mbp, np0, wp;
+          work_item(p, pair, npairs, S, it - 1, tp, s0p, s1p);
+          item_coords(p, pair, it - 1, tp, mbp, np0, wp);
+          const int c0 = (int)acc_col(acc ^ 1, wp), c1 = (int)acc_col(acc, w);
+          ovl = max(c0, c1) < min(c0 + wp, c1 + w);
+        }
         // the item's N in the instruction descriptor (bits 17-22: N >> 3); an item that
         // starts 64 rows into a W scale atom reads SFB two TMEM words in
         const uint32_t nfield = ~(0x3Fu << 17), nbits = (uint32_t)(w >> 3) << 17;
         const uint32_t sfb_off = (nt0 & 127) ? 2u : 0u;
         ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), ((it >> 1) & 1) ^ 1, 22, it, t);   // tile it-2 drained acc
         if (trace && it == 1) g_trace[blockIdx.x][16] = ptx::globaltimer_ns();
-        if (it > 0) ptx::mbar_wait(ptx::smem_u32(&tovl[acc ^ 1]), ((it - 1) >> 1) & 1, 25, it, t);  // overlap of it-1
+        if (ovl) ptx::mbar_wait(ptx::smem_u32(&tovl[acc ^ 1]), ((it - 1) >> 1) & 1, 25, it, t);  // overlap of it-1
         if (trace && it < 3) g_trace[blockIdx.x][3 + 2 * it] = ptx::globaltimer_ns();
         if (trace && it == 0) g_trace[blockIdx.x][13] = clock64();
         if (trace && it == 1) g_trace[blockIdx.x][22] = clock64();
@@ -480,9 +493,9 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       if (trace && q == 0 && it == 0 && rank == 0) g_trace[blockIdx.x][21] = clock64();
       ptx::tc_fence_after();
       const int row0 = mb2 * 256 + 128 * (int)rank + q * 32;
-      const uint32_t acc_col = acc ? ACC1_COL : 0;
+      const uint32_t acc_c = acc_col(acc, w);
       uint32_t rn[32];   // chunk 1 of the drain order, loaded together with chunk 0
-      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc_col;
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc_c;
       if (p.helpers && it == n_items - 1 && !(p.dbg & 4)) {
         // last tile: warps 0-3 drain chunks 4-7 (drain_chunks below); these warps drain
         // 0-3 into private staging buffers in the (now idle) operand ring.  The helpers
@@ -623,7 +636,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     ptx::mbar_wait_sleep(ptx::smem_u32(hgo), 0, 26, it, t);
     ptx::tc_fence_after();
     const int q = warp & 3;
-    const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + (acc ? ACC1_COL : 0);
+    const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc_col(acc, w);
     drain_chunks<NP>(tys, p.ndst, trow, sA + q * 8192, 4, w / 32, n0, mb2 * 256 + 128 * (int)rank + q * 32, lane);
     if (lane == 0) {
       if constexpr (NP == 1) ptx::bulk_wait_group_read<0>();
