@@ -91,6 +91,7 @@ struct Gemm2Dev {
   uint16_t* y_mc;        // NVLS: multicast view of all ranks' Y (nullptr: TMA stores)
   int64_t mc_col_off;    // this rank's column offset in the full Y
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
+  int sfb_mc;  // 1: W scale row groups multicast across the pair (one TMA per CTA instead of two)
   int sched2;  // 1: two-wave item table (build_split2): every pair one whole tile + at most one narrow item
   uint32_t item[2 * kMaxPairs];   // [pair][2]: bit 31 valid | mb2 | (n0 / 64) << 10 | (w / 64) << 24
 };
@@ -316,9 +317,16 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
             } else if (!no_sf) {
               ptx::tma_load_2d_cg2(ptx::smem_u32(sSFA + stage * SFA_BYTES), tsa, fb, 0, mgrp * kp128 + atom0);
 #pragma unroll
-              for (int rg = 0; rg < 2; ++rg)
-                ptx::tma_load_2d_cg2(ptx::smem_u32(sSFB + stage * SFB_BYTES + rg * 1024), tsb, fb, 0,
-                                     (rgb + rg) * kp128 + atom0);
+              if (p.sfb_mc) {
+                // both CTAs need all 256 W rows' scales: each loads its own row group ONCE and
+                // multicasts it to the pair (both deliveries complete on the leader's barrier)
+                ptx::tma_load_2d_cg2_mc(ptx::smem_u32(sSFB + stage * SFB_BYTES + (int)rank * 1024), tsb, fb, 0,
+                                        (rgb + (int)rank) * kp128 + atom0, (uint16_t)0x3);
+              } else {
+                for (int rg = 0; rg < 2; ++rg)
+                  ptx::tma_load_2d_cg2(ptx::smem_u32(sSFB + stage * SFB_BYTES + rg * 1024), tsb, fb, 0,
+                                       (rgb + rg) * kp128 + atom0);
+              }
             }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
@@ -794,6 +802,7 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   const int grid = pair_grid(a, cfg);
   const int npairs = grid / 2;
   p.stream_k = use_stream_k(a, cfg) ? 1 : 0;
+  { const char* e = getenv("MM_GEMM_SFBMC"); p.sfb_mc = e ? atoi(e) : 1; }
   {
     // two-wave schedule (build_split2) for a ragged second wave; MM_GEMM_SPLIT2=0/1 forces it
     const char* e = getenv("MM_GEMM_SPLIT2");
