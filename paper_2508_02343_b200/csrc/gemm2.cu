@@ -26,6 +26,7 @@
 #include <mutex>
 #include <utility>
 #include <vector>
+#include <tuple>
 #include <algorithm>
 
 #include "internal.h"
@@ -92,8 +93,11 @@ struct Gemm2Dev {
   int64_t mc_col_off;    // this rank's column offset in the full Y
   int dbg;   // timing experiments only (env MM_GEMM_DEBUG): 2 = no MMA, 4 = no epilogue stores
   int sfb_mc;  // 1: W scale row groups multicast across the pair (one TMA per CTA instead of two)
-  int sched2;  // 1: two-wave item table (build_split2): every pair one whole tile + at most one narrow item
-  uint32_t item[2 * kMaxPairs];   // [pair][2]: bit 31 valid | mb2 | (n0 / 64) << 10 | (w / 64) << 24
+  int sched2;  // 1: balanced schedule (build_sched): sq whole tiles per pair + at most one narrow item
+  int sq;      // whole tiles per pair
+  int npairs;  // pairs of the grid
+  uint16_t a_pref[65];            // whole tiles enumerated row-block-major: first index of row block b
+  uint32_t narrow[kMaxPairs];     // [pair]: bit 31 valid | mb2 | (n0 / 64) << 10 | (w / 64) << 24
 };
 
 // Tile raster: groups of up to 8 pair-row blocks (2048 rows of A) sweep all of N
@@ -117,7 +121,7 @@ __device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int ra
 // order, so every pair writes its partial head first and the finisher of that
 // tile -- the next pair, at the end of its own range -- finds it ready.
 __device__ __forceinline__ int num_items(const Gemm2Dev& p, int pair, int npairs, int S) {
-  if (p.sched2) return (int)(p.item[2 * pair] >> 31) + (int)(p.item[2 * pair + 1] >> 31);
+  if (p.sched2) return p.sq + (int)(p.narrow[pair] >> 31);
   if (!p.stream_k) return (p.num_tiles - pair + npairs - 1) / npairs;
   const int64_t W = (int64_t)p.num_tiles * S;
   const int64_t lo = pair * W / npairs, hi = (pair + 1) * W / npairs;
@@ -135,12 +139,22 @@ __device__ __forceinline__ void work_item(const Gemm2Dev& p, int pair, int npair
 }
 
 // Output block of item i of a pair: rows [256 mb2, +256), columns [n0, n0 + w).  Whole
-// tiles (w = 256) in the data-parallel / stream-K schedules; in the two-wave schedule
-// (p.sched2) a pair's second item may be 64 / 128 / 192 columns wide and start 64 rows
-// into a W scale atom (its MMAs then read SFB two TMEM words in; see build_split2).
+// tiles (w = 256) in the data-parallel / stream-K schedules; in the balanced schedule
+// (p.sched2) a pair's items are sq whole tiles and then at most one narrow item of 64 /
+// 128 / 192 columns that may start 64 rows into a W scale atom (its MMAs then read SFB
+// two TMEM words in; see build_sched).
 __device__ __forceinline__ void item_coords(const Gemm2Dev& p, int pair, int i, int t, int& mb2, int& n0, int& w) {
   if (p.sched2) {
-    const uint32_t e = p.item[2 * pair + i];
+    if (i < p.sq) {   // whole tile pair + i * npairs of the row-block-major enumeration
+      const int tw = pair + i * p.npairs;
+      int lo = 0, hi = p.num_m2;   // last row block b with a_pref[b] <= tw
+      while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (p.a_pref[mid] <= tw) lo = mid; else hi = mid; }
+      mb2 = lo;
+      n0 = (tw - p.a_pref[lo]) * 256;
+      w = 256;
+      return;
+    }
+    const uint32_t e = p.narrow[pair];
     mb2 = (int)(e & 1023u);
     n0 = (int)((e >> 10) & 4095u) * 64;
     w = (int)((e >> 24) & 7u) * 64;
@@ -316,7 +330,6 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
               ptx::tma_load_2d_cg2(ptx::smem_u32(sB + stage * B_BYTES), tb, fb, kcoord, n0);
             } else if (!no_sf) {
               ptx::tma_load_2d_cg2(ptx::smem_u32(sSFA + stage * SFA_BYTES), tsa, fb, 0, mgrp * kp128 + atom0);
-#pragma unroll
               if (p.sfb_mc) {
                 // both CTAs need all 256 W rows' scales: each loads its own row group ONCE and
                 // multicasts it to the pair (both deliveries complete on the leader's barrier)
@@ -694,48 +707,73 @@ bool use_stream_k(const GemmArgs& a, const GemmConfig& cfg) {
          num_tiles > npairs && num_tiles % npairs != 0 && num_tiles < 4 * npairs;
 }
 
-// Two-wave schedule for a ragged second wave (P pairs < T tiles < 2 P, e.g. q_proj: 128
-// tiles on 74 pairs).  Every pair takes ONE whole 256 x 256 tile; what is left of each
-// 256-row block (its columns past the whole tiles) is cut into narrow items of wn 64-column
-// units (wn <= 3: 192 columns, so an item that starts 64 rows into a W scale atom still
-// spans two row groups), at most one per pair.  The whole tiles per row block a_b are
-// chosen by a small DP so that the leftover splits into few items: q_proj ends with 6 row
-// blocks of 10 tiles + 8 items and 2 of 7 tiles + 12 items = 74 tiles + 72 items of 192
-// columns, i.e. no pair computes more than 448 columns instead of two 256-column tiles.
-// A narrow item still reads the whole 128-row A slab per stage, so it costs more than its
-// share of columns; the schedule is used only when it balances the work (see run2).
-bool build_split2(int num_m2, int64_t N, int P, uint32_t* item) {
+// Balanced schedule for a ragged last wave (T whole tiles = q P + r with 0 < r < P, q >= 1;
+// e.g. q_proj: 128 tiles on 74 pairs, qkv at M = 2048: 192 tiles).  Every pair takes q
+// whole 256 x 256 tiles; what is left of each 256-row block (its columns past the whole
+// tiles) is cut into narrow items of wn 64-column units (wn <= 3: 192 columns, so an item
+// that starts 64 rows into a W scale atom still spans two row groups), at most one per
+// pair, instead of r pairs computing a (q+1)-th whole tile while the others idle.  The
+// whole tiles per row block a_b (summing to q P) come from a small DP that minimises the
+// item count; q_proj ends with 74 whole tiles + 72 items of 192 columns (no pair above
+// 448 columns instead of two whole tiles).  A narrow item still reads the whole 128-row
+// A slab per stage, so it costs more than its share of columns (~81 % of a tile for 75 %
+// of its columns at 192).  Results are cached per (row blocks, N, pairs).
+struct Sched {
+  bool ok = false;
+  int q = 0;
+  std::vector<uint16_t> a_pref;
+  std::vector<uint32_t> narrow;
+};
+Sched build_sched_uncached(int num_m2, int64_t N, int P) {
+  Sched r;
   const int U = (int)((N + 63) / 64);   // 64-column units per row block
   const int A = U / 4;                  // whole tiles per row block
-  if (P < 1 || P > kMaxPairs || (int64_t)num_m2 * A < P || (int64_t)num_m2 * U <= 4LL * P || num_m2 > 64) return false;
+  const int64_t T = (int64_t)num_m2 * ((N + 255) / 256);
+  if (P < 1 || P > kMaxPairs || num_m2 > 64 || T <= P || T % P == 0) return r;
+  const int q = (int)(T / P), QP = q * P;
+  // Whole tiles are enumerated row-block-major here, not in the 8-row-block raster of the
+  // data-parallel schedule; with many waves that costs more L2 reuse than the balanced
+  // last wave gains (gate_up at M = 2048, q = 12: 142.5 -> 157.9 us), so few waves only.
+  if (q > 3) return r;
+  // (bounded host work: the DP runs once per shape, on the first call)
+  if ((int64_t)num_m2 * A < QP || (int64_t)num_m2 * (QP + 1) * (A + 1) > 4000000) return r;
   for (int wn = 1; wn <= 3; ++wn) {
-    // dp[b + 1][s]: fewest items over row blocks 0..b using s whole tiles; choice[b][s] = a_b
+    // dp[b + 1][s]: fewest items over row blocks 0..b using s whole tiles; ch[b][s] = a_b
     const int INF = 1 << 29;
-    std::vector<std::vector<int>> dp(num_m2 + 1, std::vector<int>(P + 1, INF)), ch(num_m2, std::vector<int>(P + 1, -1));
+    std::vector<std::vector<int>> dp(num_m2 + 1, std::vector<int>(QP + 1, INF)), ch(num_m2, std::vector<int>(QP + 1, -1));
     dp[0][0] = 0;
     for (int b = 0; b < num_m2; ++b)
-      for (int s0 = 0; s0 <= P; ++s0) {
+      for (int s0 = 0; s0 <= QP; ++s0) {
         if (dp[b][s0] >= INF) continue;
-        for (int a = 0; a <= A && s0 + a <= P; ++a) {
+        for (int a = 0; a <= A && s0 + a <= QP; ++a) {
           const int v = dp[b][s0] + (U - 4 * a + wn - 1) / wn;
           if (v < dp[b + 1][s0 + a]) { dp[b + 1][s0 + a] = v; ch[b][s0 + a] = a; }
         }
       }
-    if (dp[num_m2][P] > P) continue;
+    if (dp[num_m2][QP] > P) continue;
     std::vector<int> a_b(num_m2);
-    for (int b = num_m2 - 1, s1 = P; b >= 0; --b) { a_b[b] = ch[b][s1]; s1 -= a_b[b]; }
-    std::vector<uint32_t> full, narrow;
-    for (int b = 0; b < num_m2; ++b) {
-      for (int k = 0; k < a_b[b]; ++k) full.push_back((uint32_t)b | (uint32_t)(4 * k) << 10 | 4u << 24);
-      for (int u = 4 * a_b[b]; u < U; u += wn) narrow.push_back((uint32_t)b | (uint32_t)u << 10 | (uint32_t)std::min(wn, U - u) << 24);
-    }
-    for (int q = 0; q < P; ++q) {
-      item[2 * q] = full[q] | 0x80000000u;
-      item[2 * q + 1] = q < (int)narrow.size() ? (narrow[q] | 0x80000000u) : 0u;
-    }
-    return true;
+    for (int b = num_m2 - 1, s1 = QP; b >= 0; --b) { a_b[b] = ch[b][s1]; s1 -= a_b[b]; }
+    r.a_pref.assign(num_m2 + 1, 0);
+    for (int b = 0; b < num_m2; ++b) r.a_pref[b + 1] = (uint16_t)(r.a_pref[b] + a_b[b]);
+    r.narrow.assign(P, 0u);
+    int k = 0;
+    for (int b = 0; b < num_m2; ++b)
+      for (int u = 4 * a_b[b]; u < U; u += wn)
+        r.narrow[k++] = 0x80000000u | (uint32_t)b | (uint32_t)u << 10 | (uint32_t)std::min(wn, U - u) << 24;
+    r.q = q;
+    r.ok = true;
+    return r;
   }
-  return false;
+  return r;
+}
+const Sched& build_sched(int num_m2, int64_t N, int P) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int64_t, int>, Sched> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(num_m2, N, P);
+  auto it = cache.find(key);
+  if (it == cache.end()) it = cache.emplace(key, build_sched_uncached(num_m2, N, P)).first;
+  return it->second;
 }
 
 template <int STAGES, int NP>
@@ -804,11 +842,20 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.stream_k = use_stream_k(a, cfg) ? 1 : 0;
   { const char* e = getenv("MM_GEMM_SFBMC"); p.sfb_mc = e ? atoi(e) : 1; }
   {
-    // two-wave schedule (build_split2) for a ragged second wave; MM_GEMM_SPLIT2=0/1 forces it
+    // balanced schedule (build_sched) for a ragged last wave; MM_GEMM_SPLIT2=0 turns it off
     const char* e = getenv("MM_GEMM_SPLIT2");
     const bool want = e ? atoi(e) == 1 : true;
-    p.sched2 = (!p.stream_k && want && p.num_tiles > npairs && p.num_tiles < 2 * npairs &&
-                build_split2(p.num_m2, a.N, npairs, p.item)) ? 1 : 0;
+    p.sched2 = 0;
+    if (!p.stream_k && want) {
+      const Sched& sc = build_sched(p.num_m2, a.N, npairs);
+      if (sc.ok) {
+        p.sched2 = 1;
+        p.sq = sc.q;
+        p.npairs = npairs;
+        for (int b = 0; b <= p.num_m2; ++b) p.a_pref[b] = sc.a_pref[b];
+        for (int q = 0; q < npairs; ++q) p.narrow[q] = sc.narrow[q];
+      }
+    }
   }
   // Helper drain of the last tile: for few tiles per pair (<= 4), where the exposed final
   // drain is a visible share of the kernel (q_proj: 27 -> 25 us); measured ~1 % slower

@@ -1,8 +1,8 @@
-"""GPU parity: the CTA-pair GEMM's two-wave schedule (gemm2.cu build_split2).
+"""GPU parity: the CTA-pair GEMM's balanced schedule (gemm2.cu build_sched).
 
-When the whole 256 x 256 tiles leave a ragged second wave (P pairs < T tiles < 2 P; q_proj:
-128 tiles on 74 pairs), every pair takes one whole tile and at most one narrow item of
-64 / 128 / 192 columns -- some starting 64 rows into a W scale atom, whose MMAs read SFB
+When the whole 256 x 256 tiles leave a ragged last wave (T = q P + r, 0 < r < P; q_proj:
+128 tiles on 74 pairs, qkv at M = 2048: 192), every pair takes q whole tiles and at most
+one narrow item of 64 / 128 / 192 columns -- some starting 64 rows into a W scale atom, whose MMAs read SFB
 two TMEM words in.  Every output element still sums its K products in the same order,
 so the result must equal the whole-tile schedule BIT FOR BIT; it is also checked against
 the oracle (Eq. 2) and on the exact-integer case (P-I(i))."""
@@ -32,7 +32,9 @@ def _gemm(x, w, plan, split2, monkeypatch):
 # 96 tiles (128-column items), ragged M and N with a partial last 64-column unit
 @pytest.mark.parametrize("M,N,n", [(2048, 4096, (2272, 1152, 672)), (2500, 2048, (96, 160, 224)),
                                    (2048, 3072, (512, 256, 256)), (1800, 2992, (1024, 0, 512)),
-                                   (1280, 4096, (0, 512, 0))])
+                                   (1280, 4096, (0, 512, 0)),
+                                   # q = 2 and q = 12 whole tiles per pair (qkv / gate_up at M = 2048)
+                                   (2048, 6144, (512, 256, 256)), (2048, 28672, (256, 128, 128))])
 def test_split2_equals_whole_tiles_and_oracle(M, N, n, monkeypatch):
     K = sum(n)
     x = gen_act(M, K, 1004, 2700 + M)
