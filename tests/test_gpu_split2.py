@@ -33,7 +33,8 @@ def _gemm(x, w, plan, split2, monkeypatch):
 @pytest.mark.parametrize("M,N,n", [(2048, 4096, (2272, 1152, 672)), (2500, 2048, (96, 160, 224)),
                                    (2048, 3072, (512, 256, 256)), (1800, 2992, (1024, 0, 512)),
                                    (1280, 4096, (0, 512, 0)),
-                                   # q = 2 and q = 12 whole tiles per pair (qkv / gate_up at M = 2048)
+                                   # q = 2 whole tiles per pair (qkv at M = 2048); q = 12 (gate_up) keeps
+                                   # the whole-tile raster (balanced schedule only for q <= 3)
                                    (2048, 6144, (512, 256, 256)), (2048, 28672, (256, 128, 128))])
 def test_split2_equals_whole_tiles_and_oracle(M, N, n, monkeypatch):
     K = sum(n)
