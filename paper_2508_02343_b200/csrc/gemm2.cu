@@ -14,10 +14,16 @@
 // (the single-CTA 128 x 256 tile needs 48 KB): the L2 -> SM traffic, which bounds
 // the single-CTA kernel, drops by a third.
 //
-// Roles (per CTA, 256 threads): warp 0 = TMA producer (operand tiles and scale
-// atoms; completions land on the even CTA's full barrier), warp 1 = MMA issuer
-// (even CTA only: tcgen05.cp of the scale atoms + the MMAs, commits multicast to
-// both CTAs), warp 2 = TMEM allocator, warps 4-7 = epilogue (tcgen05.ld -> BF16).
+// Roles (per CTA, 256 threads): warp 0 = TMA producer of the operand tiles (posts the
+// stage's transaction count on the even CTA's full barrier), warp 3 = TMA producer of
+// the scale atoms (own SFA rows; one W scale row group, multicast to the pair), warp 1 =
+// MMA issuer (even CTA only: tcgen05.cp of the scale atoms + the MMAs, commits multicast
+// to both CTAs), warp 2 = TMEM allocator, warps 4-7 = epilogue (tcgen05.ld -> BF16 ->
+// TMA store); warps 0-3 help drain the last item.
+//
+// Schedules: whole 256 x 256 tiles round-robin over the pairs in an 8-row-block raster
+// (data-parallel); for a ragged last wave with few waves, the balanced schedule
+// (build_sched: q whole tiles + at most one narrow item per pair); opt-in stream-K.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
