@@ -373,6 +373,30 @@ template <int R> struct ChunkCtx {
 
 __device__ __forceinline__ int sel3(int g, int x0, int x1, int x2) { return g == 0 ? x0 : (g == 1 ? x1 : x2); }
 
+// Encode + stores of one block row set for a chunk whose blocks all lie in segment G
+// (first block of the segment: bseg; fmt_a: E3M2 for G = 1, E4M3 for G = 2).
+template <int R, int G>
+__device__ __forceinline__ void encode_uniform(const RqArgs& a, const typename Slot<R>::T (&v)[16],
+                                               const uint32_t (&am)[4], int b, int h, unsigned r0, unsigned sf_row,
+                                               int bseg, int nvalid, bool live, bool store_sf, bool fmt_a) {
+  constexpr int hb = G == 0 ? 8 : (G == 1 ? 12 : 16);
+  const int kb = b - bseg;
+  const uint32_t pitch = (uint32_t)a.geom.pitch[G];
+  uint8_t* crow0 = a.codes[G] + (uint64_t)r0 * pitch + (unsigned)(h * hb) + (unsigned)kb * (2 * hb);
+  uint8_t* sfp = a.sf[G] + (size_t)((r0 >> 7) * ((unsigned)a.geom.kp[G] >> 7) + ((unsigned)kb >> 2)) * 512 + sf_row +
+                 (kb & 3);
+  const int off = a.geom.sc_off[G];
+  if constexpr (G == 0) {
+    quantize_rows<R, 0, F_E2M1, 16>(v, am, off, crow0, pitch, sfp, nvalid, live, store_sf);
+  } else if constexpr (G == 1) {
+    if (fmt_a) quantize_rows<R, 1, F_E3M2, 16>(v, am, off, crow0, pitch, sfp, nvalid, live, store_sf);
+    else quantize_rows<R, 1, F_E2M3, 16>(v, am, off, crow0, pitch, sfp, nvalid, live, store_sf);
+  } else {
+    if (fmt_a) quantize_rows<R, 2, F_E4M3, 16>(v, am, off, crow0, pitch, sfp, nvalid, live, store_sf);
+    else quantize_rows<R, 2, F_E5M2, 16>(v, am, off, crow0, pitch, sfp, nvalid, live, store_sf);
+  }
+}
+
 // The chunks of one tile owned by this warp (chunk c_first, c_first + group_warps, ...).
 // A chunk is 16 consecutive 32-channel blocks of the REORDERED row -- the segments are
 // contiguous there (FP4 blocks, then FP6, then FP8) -- so a K = 4096 row is 8 chunks
@@ -452,6 +476,21 @@ __device__ __forceinline__ void tile_chunks(const RqArgs& a, const ChunkCtx<R>& 
     }
     uint32_t am[4];
     block_amax<16>(v, am);   // every lane of the warp (full-warp shuffle), before any divergence
+    const bool store_sf = live && h == 0;
+    if (MM_RQ_EXPERIMENTS && (cx.dbg & 8)) continue;            // experiment: no encode, no stores
+    // One-row tiles: the segment of the chunk's first and last live block are equal
+    // (warp-uniform) except in the chunks that straddle a segment boundary -- uniform
+    // chunks take a path whose segment geometry is compile-time (uniform registers, no
+    // per-lane selects): C4 145.5 -> 142.0 us.  For two-row tiles the extra code and
+    // registers (68 -> 74) cost more than the selects (b8 q/o 38.7 -> 39.3 us): off there.
+    const int bl0 = c * 16, bl1 = min(c * 16 + 15, nbt - 1);
+    const int g0 = bl0 < b1 ? 0 : (bl0 < b2 ? 1 : 2), g1 = bl1 < b1 ? 0 : (bl1 < b2 ? 1 : 2);
+    if (R == 1 && g0 == g1) {
+      if (g0 == 0) encode_uniform<R, 0>(a, v, am, b, h, r0, sf_row, 0, cx.nvalid, live, store_sf, true);
+      else if (g0 == 1) encode_uniform<R, 1>(a, v, am, b, h, r0, sf_row, b1, cx.nvalid, live, store_sf, e3m2);
+      else encode_uniform<R, 2>(a, v, am, b, h, r0, sf_row, b2, cx.nvalid, live, store_sf, e4m3);
+      continue;
+    }
     const int g = b < b1 ? 0 : (b < b2 ? 1 : 2);
     const int kb = b - sel3(g, 0, b1, b2);                      // block inside its segment
     const int hb = sel3(g, 8, 12, 16);                          // code bytes per half block
@@ -462,8 +501,6 @@ __device__ __forceinline__ void tile_chunks(const RqArgs& a, const ChunkCtx<R>& 
     uint8_t* const sf = g == 0 ? a.sf[0] : (g == 1 ? a.sf[1] : a.sf[2]);
     uint8_t* crow0 = codes + (uint64_t)r0 * pitch + (unsigned)(h * hb) + (unsigned)kb * (2 * hb);
     uint8_t* sfp = sf + (size_t)((r0 >> 7) * ((unsigned)kp >> 7) + ((unsigned)kb >> 2)) * 512 + sf_row + (kb & 3);
-    const bool store_sf = live && h == 0;
-    if (MM_RQ_EXPERIMENTS && (cx.dbg & 8)) continue;            // experiment: no encode, no stores
     if (g == 0) {
       quantize_rows<R, 0, F_E2M1, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
     } else if (g == 1) {
