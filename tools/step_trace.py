@@ -20,6 +20,8 @@ from synth import gen_act, gen_weight  # noqa: E402
 
 M, K, N = 2048, 4096, 4096
 dev = torch.device("cuda", 0)
+if os.environ.get("STAGES"):   # GEMM ring depth (4 / 5 / 6)
+    mm.mm_set_gemm_config(0, int(os.environ["STAGES"]), 0)
 plan = mm.mm_calibrate_thresholds(gen_act(16384, K, 1000, 2000).to(dev))
 x = gen_act(M, K, 1000, 2001, device=dev)
 wq = mm.mm_quantize_weight_offline(gen_weight(N, K, 3000, device=dev), plan)
