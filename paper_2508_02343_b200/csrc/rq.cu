@@ -977,6 +977,13 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
     groups = (int)tpc;
     gw = W / groups;
     if (gw > nch) gw = nch;
+  } else if (tpc <= 32 && groups > 7) {
+    // A few rounds of tiles per CTA (M up to ~8192 at K = 4096): the last round's latency
+    // matters more than the lookahead -- 7 groups of 3 warps instead of 10 of 2 (M = 4096:
+    // 13.43 -> 12.86 us, M = 8192: 22.21 -> 21.77 us; M = 16384, 55 tiles per CTA, keeps 10)
+    groups = 7;
+    gw = W / groups;
+    if (gw > nch) gw = nch;
   }
   { const char* e = getenv("MM_RQ_GW"); if (e && atoi(e) >= 1 && atoi(e) <= W) { gw = atoi(e); groups = W / gw; } }   // tuning
   { const char* e = getenv("MM_RQ_GROUPS"); if (e && atoi(e) >= 1 && atoi(e) <= W) { groups = atoi(e); gw = W / groups; if (gw > nch) gw = nch; } }
