@@ -985,10 +985,20 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
     gw = W / groups;
     if (gw > nch) gw = nch;
   }
-  { const char* e = getenv("MM_RQ_GW"); if (e && atoi(e) >= 1 && atoi(e) <= W) { gw = atoi(e); groups = W / gw; } }   // tuning
+  const char* gw_env = getenv("MM_RQ_GW");   // tuning
+  if (gw_env && atoi(gw_env) >= 1 && atoi(gw_env) <= W) { gw = atoi(gw_env); groups = W / gw; } else gw_env = nullptr;
   { const char* e = getenv("MM_RQ_GROUPS"); if (e && atoi(e) >= 1 && atoi(e) <= W) { groups = atoi(e); gw = W / groups; if (gw > nch) gw = nch; } }
   if (groups > max_groups) groups = max_groups;
   if (groups < 1) groups = 1;
+  if (!gw_env) {
+    // Group width: the fewest warps that still give the fewest chunk rounds per tile
+    // (ceil(nch / gw)), within the register budget -- K = 28672: 14 warps, 4 rounds
+    // (was 12 warps, 5 rounds: 142.4 -> 140.7 us); K = 27648: 141.6 -> 135.3 us.
+    const int gmax = W / groups > 0 ? W / groups : 1;
+    const int best_rounds = (nch + gmax - 1) / gmax;
+    gw = gmax;
+    while (gw > 1 && (nch + gw - 2) / (gw - 1) == best_rounds) --gw;
+  }
   d.group_warps = gw;
   d.groups = groups;
   { const char* e = getenv("MM_RQ_DEBUG"); d.dbg = e ? atoi(e) : 0; }
