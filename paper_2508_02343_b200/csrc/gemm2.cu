@@ -62,7 +62,7 @@ constexpr int ACC1_COL = 208;
 // An item of <= 208 columns in the odd accumulator sits at column 256 instead: it does not
 // overlap the even accumulator at all, so its MMAs need not wait for the previous item's
 // overlap columns to drain (that wait idles the tensor pipe for the previous item's MMA
-// completion + first TMEM loads, ~1 us between the two items of the two-wave schedule).
+// completion + first TMEM loads, ~1 us between the whole tile and the narrow item of the balanced schedule).
 __host__ __device__ constexpr uint32_t acc_col(int acc, int w) { return acc == 0 ? 0u : (w <= 208 ? 256u : (uint32_t)ACC1_COL); }
 constexpr int SF_COL = 464;
 // epilogue staging: 4 warps x NB buffers x (32 x 32 BF16); one buffer per warp when

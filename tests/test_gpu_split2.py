@@ -52,7 +52,7 @@ def test_split2_equals_whole_tiles_and_oracle(M, N, n, monkeypatch):
 
 def test_split2_exact_integer_bit_exact(monkeypatch):
     """Integer operands exact in every format (products and sums < 2^24): Y must equal
-    bf16(X W^T) bit for bit under the two-wave schedule at the q_proj tile count."""
+    bf16(X W^T) bit for bit under the balanced schedule at the q_proj tile count."""
     M, N, n = 2048, 4096, (512, 256, 256)
     rng = np.random.default_rng(7)
     K = sum(n)

@@ -1,6 +1,6 @@
 """Small launches of every kernel for compute-sanitizer (SURVEY §4.2 tier T3):
 racecheck / synccheck / memcheck / initcheck over the RQ (plain and fused RMSNorm),
-the CTA-pair GEMM (config 1, 256^3 and the two-wave schedule; W scales multicast across
+the CTA-pair GEMM (config 1, 256^3 and the balanced schedule; W scales multicast across
 the pair), the single-CTA tile GEMM, the small-M
 split-K GEMM (arrival counters), the opt-in stream-K schedule (per-warp flags) and
 the fused all-gather epilogue with 2 virtual ranks + the flag barrier.
@@ -85,7 +85,7 @@ if __name__ == "__main__":
     case("tile GEMM bn=256 M=100 N=512", lambda: gemm(100, 512, (256, 128, 128), bn=256))
     case("small-M split-K M=16 N=4096 K=4096", lambda: gemm(16, 4096, (2240, 1184, 672)))
     case("stream-K M=2560 N=2048 K=256", lambda: gemm(2560, 2048, (128, 64, 64), env={"MM_GEMM_STREAMK": "1"}))
-    case("two-wave schedule M=2560 N=2048 K=256 (64-column items)", lambda: gemm(2560, 2048, (128, 64, 64)))
-    case("two-wave schedule M=2048 N=4096 K=256 (192-column items, SFB offset)", lambda: gemm(2048, 4096, (128, 64, 64)))
+    case("balanced schedule M=2560 N=2048 K=256 (64-column items)", lambda: gemm(2560, 2048, (128, 64, 64)))
+    case("balanced schedule M=2048 N=4096 K=256 (192-column items, SFB offset)", lambda: gemm(2048, 4096, (128, 64, 64)))
     case("peer-store 2 virtual ranks + barrier", peerstore)
     print("all cases ok")
