@@ -93,7 +93,7 @@ struct Gemm2Dev {
   int* ws_flag;                   // [npairs][8 epilogue warps]: 1 = that warp's 32 partial rows are
                                   // published; the one reader warp resets it to 0 after consuming
   int ndst;  // output maps used (1, or the peer window's world size)
-  int raster;  // pair-row blocks per raster group (8; MM_GEMM_RASTER for tuning)
+  int raster;  // pair-row blocks per raster group (8, or 16 for >= 64 column tiles; MM_GEMM_RASTER for tuning)
   int helpers; // 1: warps 0-3 drain half of the LAST tile's accumulator (data-parallel schedule)
   uint16_t* y_mc;        // NVLS: multicast view of all ranks' Y (nullptr: TMA stores)
   int64_t mc_col_off;    // this rank's column offset in the full Y
@@ -841,7 +841,13 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
   p.y_mc = a.y_mc;
   p.mc_col_off = a.y_col_off;
   { const char* d = getenv("MM_GEMM_DEBUG"); p.dbg = d ? atoi(d) : 0; }
-  { const char* r = getenv("MM_GEMM_RASTER"); p.raster = (r && atoi(r) > 0) ? atoi(r) : 8; }
+  {
+    // raster groups of 8 pair-row blocks; 16 for very wide layers (>= 64 column tiles:
+    // gate_up at M = 16384 1088 -> 1065 us, Qwen gate_up N = 55296 1263 -> 1232 us; the
+    // N <= 8192 layers measured 0.2-1.8 % slower with 16, so they keep 8)
+    const char* r = getenv("MM_GEMM_RASTER");
+    p.raster = (r && atoi(r) > 0) ? atoi(r) : (p.num_n >= 64 ? 16 : 8);
+  }
   if (p.num_tiles == 0) return cudaSuccess;
   const int grid = pair_grid(a, cfg);
   const int npairs = grid / 2;
