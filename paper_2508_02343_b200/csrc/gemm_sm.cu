@@ -173,16 +173,24 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
       ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase, 32, s, nt);
       if (trace && lane == 0 && (s == s_lo || s == s_fin)) g_sm_trace[blockIdx.x][s == s_lo ? 2 : 3] = ptx::globaltimer_ns();
       ptx::tc_fence_after();
-      if (lane == 0) {
-        const uint32_t sfw_t = tmem_base + BNM + stage * C::SF_STRIDE;
-        const uint32_t sfa_t = sfw_t + 8;
-        const uint32_t sf = ptx::smem_u32(sSF + stage * 2 * C::SF_BYTES);
+      const uint32_t sfw_t = tmem_base + BNM + stage * C::SF_STRIDE;
+      const uint32_t sfa_t = sfw_t + 8;
+      const uint32_t sf = ptx::smem_u32(sSF + stage * 2 * C::SF_BYTES);
+      const uint32_t w_base = ptx::smem_u32(sW + stage * W_BYTES);
+      const uint32_t a_base = ptx::smem_u32(sA + stage * C::A_BYTES);
+      if (si.nmma == 4) {
+        // full stage: one issue block (elect.sync, scale copies, 4 MMAs, commit)
+        const uint64_t wd = ptx::smem_desc(w_base, 16, 1024, 2), ad = ptx::smem_desc(a_base, 16, 1024, 2);
+        const uint64_t sdw = ptx::smem_desc(sf, 0, 128, 0), sda = ptx::smem_desc(sf + C::SF_BYTES, 0, 128, 0);
+        const uint32_t accum = s > s_lo ? 1u : 0u;
+        if (si.g == 0) ptx::stage_f4_cg1(tmem_base, wd, ad, p.idesc[0], sfw_t, sfa_t, sdw, sda, accum, ptx::smem_u32(&empty[stage]));
+        else ptx::stage_f8f6_cg1(tmem_base, wd, ad, p.idesc[si.g], sfw_t, sfa_t, sdw, sda, accum, ptx::smem_u32(&empty[stage]));
+      } else if (lane == 0) {
+        // a segment's partial last stage: the atoms it uses, then nmma MMAs
         for (int at = 0; at < si.atoms; ++at) {
           ptx::tc_cp_32x128b_x4(sfw_t + 4 * at, ptx::smem_desc(sf + at * 512, 0, 128, 0));
           ptx::tc_cp_32x128b_x4(sfa_t + 4 * at, ptx::smem_desc(sf + C::SF_BYTES + at * 512, 0, 128, 0));
         }
-        const uint32_t w_base = ptx::smem_u32(sW + stage * W_BYTES);
-        const uint32_t a_base = ptx::smem_u32(sA + stage * C::A_BYTES);
         for (int k = 0; k < si.nmma; ++k) {
           const uint64_t wd = ptx::smem_desc(w_base + 32 * k, 16, 1024, 2);
           const uint64_t ad = ptx::smem_desc(a_base + 32 * k, 16, 1024, 2);
@@ -196,8 +204,9 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
           }
         }
         ptx::tc_commit(ptx::smem_u32(&empty[stage]));
-        if (s == s_fin) ptx::tc_commit(ptx::smem_u32(tfull));
       }
+      __syncwarp();
+      if (s == s_fin && lane == 0) ptx::tc_commit(ptx::smem_u32(tfull));
       __syncwarp();
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
