@@ -208,9 +208,25 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
         const StageInfo si = stage_info(p, s);
         ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase, 3, s, t);
         ptx::tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sfa_t = tmem_base + C::SF_BASE + stage * C::SF_STRIDE;
-          const uint32_t sfb_t = sfa_t + 8;
+        const uint32_t sfa_t = tmem_base + C::SF_BASE + stage * C::SF_STRIDE;
+        const uint32_t sfb_t = sfa_t + 8;
+        const uint32_t a_base = ptx::smem_u32(sA + stage * C::A_BYTES);
+        const uint32_t b_base = ptx::smem_u32(sB + stage * C::B_BYTES);
+        if (si.nmma == 4 && !p.dbg) {
+          // full stage: one issue block (elect.sync, scale copies, 4 MMAs, commit)
+          const uint64_t ad = ptx::smem_desc(a_base, 16, 1024, 2), bd = ptx::smem_desc(b_base, 16, 1024, 2);
+          const uint64_t sda = ptx::smem_desc(ptx::smem_u32(sSFA + stage * C::SFA_BYTES), 0, 128, 0);
+          const uint64_t sdb = ptx::smem_desc(ptx::smem_u32(sSFB + stage * C::SFB_BYTES), 0, 128, 0);
+          const uint32_t accum = s > 0 ? 1u : 0u;
+          const uint32_t eb = ptx::smem_u32(&empty[stage]);
+          if constexpr (C::RG == 1) {
+            if (si.g == 0) ptx::stage_f4_cg1(d_t, ad, bd, p.idesc[0], sfa_t, sfb_t, sda, sdb, accum, eb);
+            else ptx::stage_f8f6_cg1(d_t, ad, bd, p.idesc[si.g], sfa_t, sfb_t, sda, sdb, accum, eb);
+          } else {
+            if (si.g == 0) ptx::stage_f4_cg1_rg2(d_t, ad, bd, p.idesc[0], sfa_t, sfb_t, sda, sdb, accum, eb);
+            else ptx::stage_f8f6_cg1_rg2(d_t, ad, bd, p.idesc[si.g], sfa_t, sfb_t, sda, sdb, accum, eb);
+          }
+        } else if (lane == 0) {
           // scale atoms -> TMEM (32 rows x 16 B each, replicated to 4 lane quadrants)
           for (int at = 0; at < si.atoms && !((p.dbg & 1) && s > 0); ++at) {
             ptx::tc_cp_32x128b_x4(sfa_t + 4 * at,
@@ -221,8 +237,6 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
                   sfb_t + at * 4 * C::RG + 4 * rg,
                   ptx::smem_desc(ptx::smem_u32(sSFB + stage * C::SFB_BYTES + (at * C::RG + rg) * 512), 0, 128, 0));
           }
-          const uint32_t a_base = ptx::smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b_base = ptx::smem_u32(sB + stage * C::B_BYTES);
           for (int k = 0; k < ((p.dbg & 2) ? 0 : si.nmma); ++k) {
             const uint64_t ad = ptx::smem_desc(a_base + 32 * k, 16, 1024, 2);
             const uint64_t bd = ptx::smem_desc(b_base + 32 * k, 16, 1024, 2);
@@ -236,8 +250,9 @@ mixgemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ 
             }
           }
           ptx::tc_commit(ptx::smem_u32(&empty[stage]));
-          if (s == nstages - 1) ptx::tc_commit(ptx::smem_u32(&tfull[acc]));
         }
+        __syncwarp();
+        if (s == nstages - 1 && lane == 0) ptx::tc_commit(ptx::smem_u32(&tfull[acc]));
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }

@@ -223,6 +223,62 @@ __device__ __forceinline__ void stage_f4_cg1(uint32_t d, uint64_t ad, uint64_t b
         "r"(sfb4), "r"(bar)
       : "memory");
 }
+// Single-CTA stages whose W scales span two 128-row groups (N = 256 tiles): SFB row
+// group r of atom a at TMEM column sfb + 4 (2a + r); in shared memory the atoms are laid
+// out [atom][row group] (512 B each), so atom 1 is 1 KB (64 descriptor units) further.
+__device__ __forceinline__ void stage_f8f6_cg1_rg2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id0, uint32_t sfa,
+                                                   uint32_t sfb, uint64_t sda, uint64_t sdb0, uint32_t accum,
+                                                   uint32_t bar) {
+  const uint32_t id1 = id0 | (1u << 29) | (1u << 4), id2 = id0 | (2u << 29) | (2u << 4), id3 = id0 | (3u << 29) | (3u << 4);
+  const uint32_t sfb4 = sfb + 4;
+  asm volatile(
+      "{\n\t.reg .pred p, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3, s1;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 acc, %8, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "add.s64 s1, %7, 32;\n\t"
+      "@p tcgen05.cp.cta_group::1.32x128b.warpx4 [%4], %6;\n\t"
+      "@p tcgen05.cp.cta_group::1.32x128b.warpx4 [%5], %7;\n\t"
+      "@p tcgen05.cp.cta_group::1.32x128b.warpx4 [%12], s1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%5], acc;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], a1, b1, %9, [%4], [%5], one;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], a2, b2, %10, [%4], [%5], one;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], a3, b3, %11, [%4], [%5], one;\n\t"
+      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%13];\n\t}"
+      ::"r"(d), "l"(ad), "l"(bd), "r"(id0), "r"(sfa), "r"(sfb), "l"(sda), "l"(sdb0), "r"(accum), "r"(id1), "r"(id2),
+        "r"(id3), "r"(sfb4), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void stage_f4_cg1_rg2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id0, uint32_t sfa,
+                                                 uint32_t sfb, uint64_t sda, uint64_t sdb0, uint32_t accum,
+                                                 uint32_t bar) {
+  const uint32_t id2 = id0 | (2u << 29) | (2u << 4);
+  const uint32_t sfa4 = sfa + 4, sfb4 = sfb + 4, sfb8 = sfb + 8, sfb12 = sfb + 12;
+  asm volatile(
+      "{\n\t.reg .pred p, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3, sa1, s01, s10, s11;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 acc, %8, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "add.s64 sa1, %6, 32;\n\tadd.s64 s01, %7, 32;\n\tadd.s64 s10, %7, 64;\n\tadd.s64 s11, %7, 96;\n\t"
+      "@p tcgen05.cp.cta_group::1.32x128b.warpx4 [%4], %6;\n\t"
+      "@p tcgen05.cp.cta_group::1.32x128b.warpx4 [%10], sa1;\n\t"
+      "@p tcgen05.cp.cta_group::1.32x128b.warpx4 [%5], %7;\n\t"
+      "@p tcgen05.cp.cta_group::1.32x128b.warpx4 [%11], s01;\n\t"
+      "@p tcgen05.cp.cta_group::1.32x128b.warpx4 [%12], s10;\n\t"
+      "@p tcgen05.cp.cta_group::1.32x128b.warpx4 [%13], s11;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], acc;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], a1, b1, %9, [%4], [%5], one;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], a2, b2, %3, [%10], [%12], one;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], a3, b3, %9, [%10], [%12], one;\n\t"
+      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%14];\n\t}"
+      ::"r"(d), "l"(ad), "l"(bd), "r"(id0), "r"(sfa), "r"(sfb), "l"(sda), "l"(sdb0), "r"(accum), "r"(id2), "r"(sfa4),
+        "r"(sfb4), "r"(sfb8), "r"(sfb12), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread.
