@@ -32,7 +32,7 @@ constexpr int W_BYTES = 128 * 128;   // 128 W rows x 128 B per stage
 constexpr int kMaxSplits = 4;
 // Timeline trace (env MM_GEMM_DEBUG & 32; mm_debug_gemm_sm_trace): per CTA
 // [start, setup done, first stage full, last stage full, MMAs done (tfull), partial written, end].
-__device__ unsigned long long g_sm_trace[1024][8];
+__device__ unsigned long long g_sm_trace[1024][10];
 
 struct SmDev {
   int64_t M, N;
@@ -263,6 +263,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
     // BF16.  A second barrier keeps every CTA's shared memory alive until all reads are
     // done.  No global workspace and no arrival counters.
     ptx::cluster_sync();
+    if (trace && threadIdx.x == 128) g_sm_trace[blockIdx.x][7] = ptx::globaltimer_ns();
     if (warp >= 4) {
       // every CTA of the cluster reduces the rows m = ks, ks + splits, ...: 8 rows x
       // up to kMaxSplits remote loads in flight per thread, summed in split order
@@ -297,6 +298,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
         }
       }
     }
+    if (trace && threadIdx.x == 128) g_sm_trace[blockIdx.x][8] = ptx::globaltimer_ns();
     ptx::cluster_sync();
   }
 
@@ -401,5 +403,5 @@ cudaError_t launch_mixed_gemm_smallm(const GemmArgs& a, const GemmConfig& cfg, c
 
 // Debug hook (not part of include/mm.h): copy the small-M GEMM trace to the host.
 extern "C" int mm_debug_gemm_sm_trace(unsigned long long* h, int n) {
-  return (int)cudaMemcpyFromSymbol(h, mmx::g_sm_trace, sizeof(unsigned long long) * (size_t)(n < 8192 ? n : 8192));
+  return (int)cudaMemcpyFromSymbol(h, mmx::g_sm_trace, sizeof(unsigned long long) * (size_t)(n < 10240 ? n : 10240));
 }

@@ -18,13 +18,13 @@ M, N = int(sys.argv[1]), int(sys.argv[2])
 n = tuple(int(v) for v in sys.argv[3].split(","))
 time_gemm(M, N, n, reps=3)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 8192)()
-mm.lib().mm_debug_gemm_sm_trace(buf, 8192)
-a = np.array(buf, dtype=np.float64).reshape(1024, 8)
+buf = (ctypes.c_ulonglong * 10240)()
+mm.lib().mm_debug_gemm_sm_trace(buf, 10240)
+a = np.array(buf, dtype=np.float64).reshape(1024, 10)
 a = a[a[:, 0] > 0]
 t0 = a[:, 0].min()
 rel = np.where(a > 0, (a - t0) / 1e3, np.nan)
-for i, nm in enumerate(["start", "setup", "first_full", "last_full", "mma_done", "partial_out", "end"]):
+for i, nm in enumerate(["start", "setup", "first_full", "last_full", "mma_done", "partial_out", "end", "cluster_sync1", "reduced"]):
     col = rel[:, i]
     col = col[~np.isnan(col)]
     if len(col):
