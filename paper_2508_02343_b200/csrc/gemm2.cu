@@ -126,16 +126,18 @@ __device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int ra
 // (this pair leaves a partial for the next pair).  Items run in DESCENDING tile
 // order, so every pair writes its partial head first and the finisher of that
 // tile -- the next pair, at the end of its own range -- finds it ready.
+template <bool LEAN = false>
 __device__ __forceinline__ int num_items(const Gemm2Dev& p, int pair, int npairs, int S) {
   if (p.sched2) return p.sq + (int)(p.narrow[pair] >> 31);
-  if (!p.stream_k) return (p.num_tiles - pair + npairs - 1) / npairs;
+  if (LEAN || !p.stream_k) return (p.num_tiles - pair + npairs - 1) / npairs;
   const int64_t W = (int64_t)p.num_tiles * S;
   const int64_t lo = pair * W / npairs, hi = (pair + 1) * W / npairs;
   return hi > lo ? (int)((hi - 1) / S - lo / S + 1) : 0;
 }
+template <bool LEAN = false>
 __device__ __forceinline__ void work_item(const Gemm2Dev& p, int pair, int npairs, int S, int i, int& t, int& s0,
                                           int& s1) {
-  if (!p.stream_k) { t = pair + i * npairs; s0 = 0; s1 = S; return; }
+  if (LEAN || !p.stream_k) { t = pair + i * npairs; s0 = 0; s1 = S; return; }
   const int64_t W = (int64_t)p.num_tiles * S;
   const int64_t lo = pair * W / npairs, hi = (pair + 1) * W / npairs;
   t = (int)((hi - 1) / S) - i;
@@ -216,7 +218,9 @@ __device__ __forceinline__ void drain_chunks(const YMaps<NP>& tys, int ndst, uin
   }
 }
 
-template <int STAGES, int NP>
+// LEAN: the default path's instantiation -- stream-K, the NVLS multicast epilogue, the
+// timeline trace and the timing-experiment switches compiled out (a smaller kernel).
+template <int STAGES, int NP, bool LEAN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                 const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb0,
@@ -245,7 +249,10 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();    // 0 = MMA leader
   const uint64_t t_start = ptx::globaltimer_ns();
-  const bool trace = (p.dbg & 32) && lane == 0;
+  const int dbg = LEAN ? 0 : p.dbg;
+  const bool streamk = !LEAN && p.stream_k;
+  uint16_t* const y_mc = LEAN ? nullptr : p.y_mc;
+  const bool trace = (dbg & 32) && lane == 0;
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
 
   if (warp == 0 && lane == 0) {
@@ -280,7 +287,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
   if (trace && warp == 1) { g_trace[blockIdx.x][0] = t_start; g_trace[blockIdx.x][1] = ptx::globaltimer_ns(); }
   const int64_t M = p.M, N = p.N;
   const int S = p.nst0 + p.nst1 + p.nst2;
-  const int n_items = num_items(p, pair, npairs, S);
+  const int n_items = num_items<LEAN>(p, pair, npairs, S);
 
   if (warp == 0 || warp == 3) {
     // ============================ TMA producers (both CTAs) ============================
@@ -295,7 +302,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       const uint32_t full0 = ptx::smem_u32(&full[0]);
       for (int it = 0; it < n_items; ++it) {
         int t, s0, s1;
-        work_item(p, pair, npairs, S, it, t, s0, s1);
+        work_item<LEAN>(p, pair, npairs, S, it, t, s0, s1);
         int mb2, nt0, w;
         item_coords(p, pair, it, t, mb2, nt0, w);
         const int m0 = mb2 * 256 + 128 * (int)rank;      // this CTA's A rows
@@ -324,8 +331,8 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
             else seg_stage<2>(p, j, kcoord, nmma, atoms, atom0);
             ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1, 21, stage, t);
             const uint32_t fb = full0 + 8 * stage;     // the even CTA's barrier (peer bit cleared)
-            const bool no_sf = (p.dbg & 8) != 0;   // timing experiment only
-            if (p.dbg & 16) {                      // timing experiment: no loads at all
+            const bool no_sf = (dbg & 8) != 0;   // timing experiment only
+            if (dbg & 16) {                      // timing experiment: no loads at all
               if (rank == 0 && ops) ptx::mbar_arrive(fb);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
               continue;
@@ -365,10 +372,10 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       const uint32_t sA0 = ptx::smem_u32(sA), sB0 = ptx::smem_u32(sB);
       const uint32_t sSFA0 = ptx::smem_u32(sSFA), sSFB0 = ptx::smem_u32(sSFB);
       const uint32_t empty0 = ptx::smem_u32(&empty[0]), full0 = ptx::smem_u32(&full[0]);
-      const bool no_mma = (p.dbg & 2) != 0;
+      const bool no_mma = (dbg & 2) != 0;
       for (; it < n_items; ++it) {
         int t, s0, s1;
-        work_item(p, pair, npairs, S, it, t, s0, s1);
+        work_item<LEAN>(p, pair, npairs, S, it, t, s0, s1);
         const int acc = it & 1;
         int mb2_, nt0, w;
         item_coords(p, pair, it, t, mb2_, nt0, w);
@@ -376,7 +383,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         bool ovl = false;   // does this item's accumulator overlap the previous item's?
         if (it > 0) {
           int tp, s0p, s1p, mbp, np0, wp;
-          work_item(p, pair, npairs, S, it - 1, tp, s0p, s1p);
+          work_item<LEAN>(p, pair, npairs, S, it - 1, tp, s0p, s1p);
           item_coords(p, pair, it - 1, tp, mbp, np0, wp);
           const int c0 = (int)acc_col(acc ^ 1, wp), c1 = (int)acc_col(acc, w);
           ovl = max(c0, c1) < min(c0 + wp, c1 + w);
@@ -418,7 +425,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
               if (g == 0) ptx::stage_f4_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage,
                                             sfb_t + sfb_off);
               else ptx::stage_f8f6_cg2(d_t, ad, bd, idesc, sfa_t, sfb_t, sda, sdb0, sdb1, accum, empty0 + 8 * stage,
-                                       (p.dbg & 64) ? 0u : 1u, sfb_t + sfb_off);
+                                       (dbg & 64) ? 0u : 1u, sfb_t + sfb_off);
               accum = 1;
             } else {
               // partial stage: scale copies for the atoms it uses, then nmma MMAs
@@ -469,7 +476,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     int nstore = 0;
     for (int it = 0; it < n_items; ++it) {
       int t, s0, s1;
-      work_item(p, pair, npairs, S, it, t, s0, s1);
+      work_item<LEAN>(p, pair, npairs, S, it, t, s0, s1);
       int mb2, n0, w;
       item_coords(p, pair, it, t, mb2, n0, w);
       const int nch = w / 32;   // 32-column chunks of this item (8 for a whole tile)
@@ -523,7 +530,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
       const uint32_t acc_c = acc_col(acc, w);
       uint32_t rn[32];   // chunk 1 of the drain order, loaded together with chunk 0
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc_c;
-      if (p.helpers && it == n_items - 1 && !(p.dbg & 4)) {
+      if (p.helpers && it == n_items - 1 && !(dbg & 4)) {
         // last tile: warps 0-3 drain chunks 4-7 (drain_chunks below); these warps drain
         // 0-3 into private staging buffers in the (now idle) operand ring.  The helpers
         // are released through their own barrier, not tfull: a phase-parity wait on tfull
@@ -569,7 +576,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
             if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
           }
         }
-        if (p.dbg & 4) continue;
+        if (dbg & 4) continue;
         if (to_ws) {   // fp32 partial -> workspace row (128 B per chunk per thread)
           float4* dst = reinterpret_cast<float4*>(p.ws + ((size_t)pair * 256 + wrow) * 256 + 32 * c);
 #pragma unroll
@@ -592,14 +599,14 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
         uint32_t w[16];
 #pragma unroll
         for (int v = 0; v < 16; ++v) w[v] = ptx::pack_bf16x2(__uint_as_float(r[2 * v]), __uint_as_float(r[2 * v + 1]));
-        if (p.y_mc) {
+        if (y_mc) {
           // NVLS: row row0 + lane, 32 columns as four 16-byte multimem stores (one write
           // per element reaches every rank's Y); rows >= M and columns >= N (the shard)
           // are clipped like the TMA boxes clip them.
           const int64_t rr = row0 + lane;
           const int col = n0 + 32 * c;
           if (rr < M) {
-            uint16_t* dst = p.y_mc + rr * p.ldy + p.mc_col_off + col;
+            uint16_t* dst = y_mc + rr * p.ldy + p.mc_col_off + col;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               if (col + 8 * k < N)
@@ -645,7 +652,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     if (trace && q == 0) g_trace[blockIdx.x][12] = ptx::globaltimer_ns();
   }
 
-  if (warp < 4 && p.helpers && n_items > 0 && !(p.dbg & 4)) {
+  if (warp < 4 && p.helpers && n_items > 0 && !(dbg & 4)) {
     // ==================== helpers: drain of the last tile ====================
     // The producer, MMA and allocator warps are idle once the last tile is issued; they
     // drain columns 128..255 of its accumulator (their TMEM lane quadrant = warp % 4)
@@ -653,7 +660,7 @@ mixgemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__
     __syncwarp();
     const int it = n_items - 1;
     int t, s0, s1;
-    work_item(p, pair, npairs, S, it, t, s0, s1);
+    work_item<LEAN>(p, pair, npairs, S, it, t, s0, s1);
     int mb2, n0, w;
     item_coords(p, pair, it, t, mb2, n0, w);
     const int acc = it & 1;
@@ -886,7 +893,8 @@ cudaError_t run2(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int64
     p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a.ws) + ws_align((size_t)npairs * 8 * sizeof(int)));
   }
   const size_t smem = 1024 + (size_t)STAGES * STAGE_BYTES + epi_bytes<STAGES>() + (2 * STAGES + 11) * 8 + 16;
-  auto kern = mixgemm2_kernel<STAGES, NP>;
+  auto kern = (NP == 1 && !p.stream_k && !p.y_mc && p.dbg == 0) ? mixgemm2_kernel<STAGES, NP, true>
+                                                                : mixgemm2_kernel<STAGES, NP, false>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
   e = launch_pdl(kern, dim3(grid), dim3(kThreads2), smem, s, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
