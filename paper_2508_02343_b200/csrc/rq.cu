@@ -406,7 +406,7 @@ __device__ __forceinline__ void encode_uniform(const RqArgs& a, const typename S
 // block's segment, which is warp-uniform except in the (at most two) chunks that
 // straddle a segment boundary.  Storage padding blocks (n_g .. kp_g) are written by
 // tile_padding.
-template <int R, bool NORM>
+template <int R, bool NORM, bool U16>
 __device__ __forceinline__ void tile_chunks(const RqArgs& a, const ChunkCtx<R>& cx, int c_first, bool e3m2,
                                             bool e4m3, const float (&rn)[4]) {
   using ST = typename Slot<R>::T;
@@ -436,7 +436,7 @@ __device__ __forceinline__ void tile_chunks(const RqArgs& a, const ChunkCtx<R>& 
     if (MM_RQ_EXPERIMENTS && (cx.dbg & 16)) continue;           // timing experiment: no stores at all
     const int bg = (MM_RQ_EXPERIMENTS && (cx.dbg & 64)) ? 0 : b;   // experiment 64: broadcast gather
     ST v[16];
-    if (cx.tab == 3) {   // u32 offsets: 4 x 128-bit table loads, slot address = stage base + offset
+    if (!U16 && cx.tab == 3) {   // u32 offsets: 4 x 128-bit table loads, slot address = stage base + offset
       const uint4* gp = reinterpret_cast<const uint4*>(cx.gidx + 32 * bg + 16 * h);
       const int rot = (cx.lane >> 1) & 3;          // the table build's per-lane rotation
 #pragma unroll
@@ -447,7 +447,7 @@ __device__ __forceinline__ void tile_chunks(const RqArgs& a, const ChunkCtx<R>& 
         v[4 * q4 + 2] = *reinterpret_cast<const ST*>(st_u + e.z);
         v[4 * q4 + 3] = *reinterpret_cast<const ST*>(st_u + e.w);
       }
-    } else if (cx.tab) {
+    } else if (U16 || cx.tab) {
       const uint4 p0 = lds_u4(tb0 + 64u * (uint32_t)bg), p1 = lds_u4(tb1 + 64u * (uint32_t)bg);
       const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
@@ -574,7 +574,9 @@ struct RqDev {
 // Thread budget per variant (register file / threads = registers per lane).
 constexpr int rq_max_threads(int R, bool NORM) { return (R == 4 || NORM) ? RQ_T4 : (R == 2 ? RQ_T2 : 1024); }
 
-template <int R, bool NORM>
+// U16: the instantiation for the default u16 gather table (table modes 1 and 2); the
+// u32 (mode 3, opt-in) and table-less (mode 0) paths compiled out -- a smaller kernel.
+template <int R, bool NORM, bool U16>
 __global__ void __launch_bounds__(rq_max_threads(R, NORM), 1)
 rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev d) {
   using ST = typename Slot<R>::T;
@@ -663,7 +665,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   // Gather table: u16 slot byte offsets, two per word, [block][16 words]: the lane
   // holding half h of block b reads words 16 b + 8 h .. + 7 with two 128-bit loads
   // (the warp reads 1 KB contiguously: conflict free).
-  const int tab = d.perm_smem;
+  const int tab = U16 ? (d.perm_smem == 1 ? 1 : 2) : d.perm_smem;
   if (tab) {
     if (tab == 1 || tab == 3) ptx::mbar_wait(ptx::smem_u32(permbar), 0, 13, 0, 0);
     const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
@@ -885,7 +887,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       const int64_t left = rows - r0;
       const int nvalid = left >= R ? R : (left > 0 ? (int)left : 0);
       const ChunkCtx<R> cx{st, smem, gidx, gamma_r, (int)r0, nvalid, group_warps, lane, dbg, tab};
-      tile_chunks<R, NORM>(a, cx, gw, e3m2, e4m3, rn);
+      tile_chunks<R, NORM, U16>(a, cx, gw, e3m2, e4m3, rn);
       if (gw == group_warps - 1 && has_pad && !(dbg & 16)) tile_padding<R>(a, (int)r0, nvalid, lane);
       if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && gw == 0 && lane == 0 && i < 6) g_rq_trace[blockIdx.x][3 + 2 * i] = ptx::globaltimer_ns();
       if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && gw == 0 && lane == 0) g_rq_trace[blockIdx.x][15] = ptx::globaltimer_ns();
@@ -1030,12 +1032,14 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   }
   const size_t norm_bytes = a.gamma ? ((size_t)a.K * 2 + 255) / 256 * 256 + 4096 : 0;
   const size_t smem = 1024 + (size_t)stages * stage_bytes + tab_bytes + norm_bytes + (2 * stages + 1) * 8;
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(rq_kernel<R, NORM>), smem);
+  const bool u16 = d.perm_smem == 1 || d.perm_smem == 2;
+  auto kern = u16 ? rq_kernel<R, NORM, true> : rq_kernel<R, NORM, false>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int threads = 32 * (1 + groups * gw);
   int64_t grid = sm_count();
   if (grid > d.n_tiles) grid = d.n_tiles;
-  e = launch_pdl(rq_kernel<R, NORM>, dim3((unsigned)grid), dim3(threads), smem, s, m, d);
+  e = launch_pdl(kern, dim3((unsigned)grid), dim3(threads), smem, s, m, d);
   if (launches) ++*launches;
   return e != cudaSuccess ? e : cudaGetLastError();
 }
