@@ -84,7 +84,9 @@ __device__ __forceinline__ SmStage sm_stage(const SmDev& p, int s) {
   return si;
 }
 
-template <int BNM, int STAGES>
+// TRACE: the timeline-trace instantiation (MM_GEMM_DEBUG & 32); the default one compiles
+// the trace stores out.
+template <int BNM, int STAGES, bool TRACE>
 __global__ void __launch_bounds__(kThreadsSm, 1)
 mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtensorMap tw1,
                   const __grid_constant__ CUtensorMap tw2, const __grid_constant__ CUtensorMap ta0,
@@ -103,7 +105,7 @@ mixgemm_sm_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const bool trace = (p.dbg & 32) && blockIdx.x < 1024;
+  const bool trace = TRACE && blockIdx.x < 1024;
   if (trace && threadIdx.x == 0) g_sm_trace[blockIdx.x][0] = ptx::globaltimer_ns();
   const int nt = blockIdx.x / p.splits, ks = blockIdx.x % p.splits;
   const int S = p.nst[0] + p.nst[1] + p.nst[2];
@@ -375,7 +377,7 @@ cudaError_t run_sm(const GemmArgs& a, const GemmConfig& cfg, cudaStream_t s, int
   p.splits = splits;
 
   const size_t smem = 1024 + (size_t)STAGES * C::STAGE_BYTES + (2 * STAGES + 1) * 8 + 16;
-  auto kern = mixgemm_sm_kernel<BNM, STAGES>;
+  auto kern = (p.dbg & 32) ? mixgemm_sm_kernel<BNM, STAGES, true> : mixgemm_sm_kernel<BNM, STAGES, false>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) { *err = "cudaFuncSetAttribute(smem) failed"; return e; }
   // the splits of one W tile form a thread-block cluster (cluster rank = split index)
