@@ -592,7 +592,10 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   // (+ the gather layout's per-line words for the transpose, R = 2 only)
   const size_t tab_core = perm_copy + ((d.perm_smem == 1 || d.perm_smem == 2) ? ((size_t)K * 2 + 15) / 16 * 16 : 0);
   const uint32_t* layout = R == 2 ? a.layout : nullptr;
-  const size_t tab_bytes = tab_core + (layout ? (size_t)d.nbox * 32 : 0);
+  // R = 2 without the norm: the transpose reads per-(box, lane) store offsets (lay_x,
+  // 32 words per box, built below); R = 2 with the norm: one layout word per 32-channel line
+  constexpr bool LX = R == 2 && !NORM;
+  const size_t tab_bytes = tab_core + (LX ? (size_t)d.nbox * 128 : (layout ? (size_t)d.nbox * 32 : 0));
   uint32_t* lay_s = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + tab_core);
   const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
   uint32_t* gidx = d.perm_smem == 3 ? reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes)   // K words
@@ -678,7 +681,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       if (!layout) return p;
       return (p & ~31u) | (((__ldg(layout + (p >> 5)) >> (4 * ((p >> 2) & 7))) & 7u) << 2) | (p & 3u);
     };
-    if (layout)   // one word per 32-channel line of every box; lines past K keep the natural order
+    if (layout && !LX)   // one word per 32-channel line of every box; lines past K keep the natural order
       for (int t = ct; t < 8 * nbox; t += cn) lay_s[t] = t < K / 32 ? __ldg(layout + t) : 0x76543210u;
     if (tab == 3) {   // in place, one 16-position group per thread: perm[j] -> slot byte offset
       for (int t = ct; t < K / 16; t += cn) {
@@ -713,7 +716,29 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
                               pv[3].z | pv[3].w << 16);
       }
     }
-    ptx::named_bar_sync(15, cn);
+  }
+  if constexpr (LX) {
+    // Transpose store offsets: for lane l of box b, the byte offsets inside the box of its two
+    // 16-byte chunks, the one stored first in the low half.  Lane l owns chunks 2 (l & 3) and
+    // 2 (l & 3) + 1 of 32-channel line l / 4; lanes 4..7 of every 8 store their odd chunk
+    // first (8 bank groups per store instruction); the chunk positions come from the plan's
+    // parity-preserving gather layout (natural order without one and past K).
+    const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
+    for (int t = ct; t < 32 * nbox; t += cn) {
+      const int l = t & 31, li = 8 * (t >> 5) + (l >> 2);
+      const uint32_t qf = 2u * (uint32_t)(l & 3) + (uint32_t)((l >> 2) & 1);
+      uint32_t pf = qf, ps = qf ^ 1u;
+      if (layout && li < K / 32) {
+        const uint32_t lw = __ldg(layout + li);
+        pf = (lw >> (4 * qf)) & 7u;
+        ps = (lw >> (4 * (qf ^ 1u))) & 7u;
+      }
+      const uint32_t base = (uint32_t)(l >> 2) * 128u;
+      lay_s[t] = (base + 16u * pf) | ((base + 16u * ps) << 16);
+    }
+  }
+  if (tab || LX) {
+    ptx::named_bar_sync(15, groups * group_warps * 32);
     if ((MM_RQ_EXPERIMENTS && (d.dbg & 32)) && threadIdx.x == 32) g_rq_trace[blockIdx.x][1] = ptx::globaltimer_ns();
   }
   ptx::grid_dep_wait();   // the outputs may still be read by the preceding kernel
@@ -743,36 +768,31 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     // registers, so the norm needs no second pass over the stage.)
     double nhi[4] = {0, 0, 0, 0}, nlo[4] = {0, 0, 0, 0};
     if constexpr (R > 1) {
-      if constexpr (R == 2 && !NORM) {
-        // Lane l owns channels 8 l .. 8 l + 7 of each box, i.e. 16-byte chunks 2 (l & 3) and
-        // 2 (l & 3) + 1 of 32-channel line l / 4.  Lanes 4..7 of every 8 store their odd
-        // chunk first, so the 8 chunks of each store instruction fill 8 different bank
-        // groups (4 wavefronts per 512 B instead of 8): the lane reads its row words as two
-        // 8-byte halves in store order (no register selects), and the chunk positions come
-        // from the plan's parity-preserving gather layout (identity past K, see lay_s).
-        const int f = (lane >> 2) & 1;
-        const int qf = 2 * (lane & 3) + f;               // chunk stored first
-        const uint32_t shf = 4u * (uint32_t)qf, shs = 4u * (uint32_t)(qf ^ 1);
+      if constexpr (LX) {
+        // Lane l owns channels 8 l .. 8 l + 7 of each box; it reads its row words as two
+        // 8-byte halves in store order (no register selects) and stores the two transposed
+        // 16-byte chunks at the offsets lay_s holds for (box, lane).  Shared addresses are
+        // 32-bit with a warp-uniform box base.
+        const uint32_t f8 = 8u * (uint32_t)((lane >> 2) & 1);
+        const uint32_t rf = (uint32_t)lane * 16u + f8, rs = (uint32_t)lane * 16u + (f8 ^ 8u);
+        const uint32_t st_b = __reduce_max_sync(0xffffffffu, ptx::smem_u32(st));
+        const uint32_t lx = ptx::smem_u32(lay_s) + 4u * (uint32_t)lane;
         for (int b = gw; b < nbox && !(dbg & 2); b += group_warps) {
-          uint8_t* box = st + b * 1024;
-          const uint2 a0 = *reinterpret_cast<const uint2*>(box + lane * 16 + 8 * f);
-          const uint2 a1 = *reinterpret_cast<const uint2*>(box + 512 + lane * 16 + 8 * f);
-          const uint2 b0 = *reinterpret_cast<const uint2*>(box + lane * 16 + 8 * (f ^ 1));
-          const uint2 b1 = *reinterpret_cast<const uint2*>(box + 512 + lane * 16 + 8 * (f ^ 1));
+          const uint32_t box = st_b + (uint32_t)b * 1024u;
+          uint2 a0, a1, b0, b1;
+          asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(a0.x), "=r"(a0.y) : "r"(box + rf));
+          asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+512];" : "=r"(a1.x), "=r"(a1.y) : "r"(box + rf));
+          asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(b0.x), "=r"(b0.y) : "r"(box + rs));
+          asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+512];" : "=r"(b1.x), "=r"(b1.y) : "r"(box + rs));
+          uint32_t w;
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w) : "r"(lx + (uint32_t)b * 128u));
           __syncwarp();
-          const uint4 cf = make_uint4(__byte_perm(a0.x, a1.x, 0x5410), __byte_perm(a0.x, a1.x, 0x7632),
-                                      __byte_perm(a0.y, a1.y, 0x5410), __byte_perm(a0.y, a1.y, 0x7632));
-          const uint4 cs = make_uint4(__byte_perm(b0.x, b1.x, 0x5410), __byte_perm(b0.x, b1.x, 0x7632),
-                                      __byte_perm(b0.y, b1.y, 0x5410), __byte_perm(b0.y, b1.y, 0x7632));
-          uint32_t pf = (uint32_t)qf, ps = (uint32_t)(qf ^ 1);
-          if (layout) {
-            const uint32_t lw = lay_s[8 * b + (lane >> 2)];
-            pf = (lw >> shf) & 7u;
-            ps = (lw >> shs) & 7u;
-          }
-          uint4* line = reinterpret_cast<uint4*>(box + (lane >> 2) * 128);
-          line[pf] = cf;
-          line[ps] = cs;
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + (w & 0xFFFFu)),
+                       "r"(__byte_perm(a0.x, a1.x, 0x5410)), "r"(__byte_perm(a0.x, a1.x, 0x7632)),
+                       "r"(__byte_perm(a0.y, a1.y, 0x5410)), "r"(__byte_perm(a0.y, a1.y, 0x7632)) : "memory");
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + (w >> 16)),
+                       "r"(__byte_perm(b0.x, b1.x, 0x5410)), "r"(__byte_perm(b0.x, b1.x, 0x7632)),
+                       "r"(__byte_perm(b0.y, b1.y, 0x5410)), "r"(__byte_perm(b0.y, b1.y, 0x7632)) : "memory");
         }
       } else
       for (int b = gw; b < nbox && !(dbg & 2); b += group_warps) {
@@ -942,7 +962,10 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   // gather layout (R = 2 with a table only): per-line words for the transpose
   static const int no_layout = [] { const char* e = getenv("MM_RQ_NO_LAYOUT"); return e ? atoi(e) : 0; }();  // A/B
   if (R != 2 || d.perm_smem == 0 || no_layout) d.a.layout = nullptr;
-  if (d.a.layout) tab_bytes += (size_t)d.nbox * 32;   // one word per 32-channel line of every box
+  // transpose offsets (R = 2 without the norm: one word per box and lane) or layout words
+  // (R = 2 with the norm: one per 32-channel line of every box)
+  if (R == 2 && !NORM) tab_bytes += (size_t)d.nbox * 128;
+  else if (d.a.layout) tab_bytes += (size_t)d.nbox * 32;
   int stages = (int)((budget - tab_bytes) / stage_bytes);
   if (stages > 32) stages = 32;
   { const char* e = getenv("MM_RQ_STAGES"); if (e && atoi(e) >= 2 && atoi(e) < stages) stages = atoi(e); }
