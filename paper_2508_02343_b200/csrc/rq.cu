@@ -549,6 +549,7 @@ struct RqDev {
   int perm_smem;        // gather table: 3 = perm bulk-copied and turned IN PLACE into u32 slot offsets;
                         // 1 = perm bulk-copied + u16 table; 2 = u16 table built from global; 0 = none (L1)
   int box3d;            // 1: one 3-D TMA per tile ({256, R, nbox} box), 0: nbox 2-D boxes
+  int lay_copy;         // 1: the gather layout's words are bulk-copied with the permutation
   int dbg;              // timing experiments only (env MM_RQ_DEBUG): 1 = skip gather/quantize, 2 = skip transpose too
 };
 
@@ -595,8 +596,13 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
   // R = 2 without the norm: the transpose reads per-(box, lane) store offsets (lay_x,
   // 32 words per box, built below); R = 2 with the norm: one layout word per 32-channel line
   constexpr bool LX = R == 2 && !NORM;
-  const size_t tab_bytes = tab_core + (LX ? (size_t)d.nbox * 128 : (layout ? (size_t)d.nbox * 32 : 0));
+  const size_t lay_bytes = LX ? (size_t)d.nbox * 128 : (layout ? (size_t)d.nbox * 32 : 0);
+  const size_t tab_bytes = tab_core + lay_bytes + (d.lay_copy ? (size_t)K / 8 : 0);
   uint32_t* lay_s = reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + tab_core);
+  // the layout's per-line words: a shared copy that arrives with the permutation, or global
+  const uint32_t* lay_w = d.lay_copy ? reinterpret_cast<const uint32_t*>(smem + (size_t)d.stages * stage_bytes +
+                                                                         tab_core + lay_bytes)
+                                     : layout;
   const int32_t* perm_s = reinterpret_cast<const int32_t*>(smem + (size_t)d.stages * stage_bytes);
   uint32_t* gidx = d.perm_smem == 3 ? reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes)   // K words
                                     : reinterpret_cast<uint32_t*>(smem + (size_t)d.stages * stage_bytes + perm_copy);  // K/2
@@ -624,8 +630,9 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tmx);
     if (d.perm_smem == 1 || d.perm_smem == 3) {  // the permutation arrives asynchronously, alongside the first tiles
-      ptx::mbar_arrive_expect_tx(ptx::smem_u32(permbar), (uint32_t)K * 4);
+      ptx::mbar_arrive_expect_tx(ptx::smem_u32(permbar), (uint32_t)K * 4 + (d.lay_copy ? (uint32_t)K / 8 : 0u));
       ptx::bulk_load(ptx::smem_u32(perm_s), a.perm, (uint32_t)K * 4, ptx::smem_u32(permbar));
+      if (d.lay_copy) ptx::bulk_load(ptx::smem_u32(lay_w), layout, (uint32_t)K / 8, ptx::smem_u32(permbar));
     }
   }
   __syncthreads();
@@ -677,9 +684,9 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     // "rotated" slot (q + rot(l)) of its own group (see tile_chunks).
     const uint32_t sz = (uint32_t)sizeof(ST);
     // slot of channel p: the layout moves 4-channel chunks inside each 32-channel line
-    auto slot = [layout](uint32_t p) -> uint32_t {
+    auto slot = [layout, lay_w](uint32_t p) -> uint32_t {
       if (!layout) return p;
-      return (p & ~31u) | (((__ldg(layout + (p >> 5)) >> (4 * ((p >> 2) & 7))) & 7u) << 2) | (p & 3u);
+      return (p & ~31u) | (((lay_w[p >> 5] >> (4 * ((p >> 2) & 7))) & 7u) << 2) | (p & 3u);
     };
     if (layout && !LX)   // one word per 32-channel line of every box; lines past K keep the natural order
       for (int t = ct; t < 8 * nbox; t += cn) lay_s[t] = t < K / 32 ? __ldg(layout + t) : 0x76543210u;
@@ -729,7 +736,7 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
       const uint32_t qf = 2u * (uint32_t)(l & 3) + (uint32_t)((l >> 2) & 1);
       uint32_t pf = qf, ps = qf ^ 1u;
       if (layout && li < K / 32) {
-        const uint32_t lw = __ldg(layout + li);
+        const uint32_t lw = lay_w[li];
         pf = (lw >> (4 * qf)) & 7u;
         ps = (lw >> (4 * (qf ^ 1u))) & 7u;
       }
@@ -966,6 +973,11 @@ cudaError_t launch_rq_t(const RqArgs& a, cudaStream_t s, int64_t* launches) {
   // (R = 2 with the norm: one per 32-channel line of every box)
   if (R == 2 && !NORM) tab_bytes += (size_t)d.nbox * 128;
   else if (d.a.layout) tab_bytes += (size_t)d.nbox * 32;
+  // the layout words travel with the permutation's bulk copy (mode 1; whole 16-byte units):
+  // the table build then reads them from shared memory, not through an L2 round trip
+  static const int no_lay_copy = [] { const char* e = getenv("MM_RQ_NO_LAYCOPY"); return e ? atoi(e) : 0; }();  // A/B
+  d.lay_copy = (d.a.layout && d.perm_smem == 1 && a.K % 128 == 0 && !no_lay_copy) ? 1 : 0;
+  if (d.lay_copy) tab_bytes += (size_t)a.K / 8;
   int stages = (int)((budget - tab_bytes) / stage_bytes);
   if (stages > 32) stages = 32;
   { const char* e = getenv("MM_RQ_STAGES"); if (e && atoi(e) >= 2 && atoi(e) < stages) stages = atoi(e); }
