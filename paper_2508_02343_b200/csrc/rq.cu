@@ -64,9 +64,19 @@ template <> struct Cvt<F_E5M2> {
 };
 // FP6: four codes -> 24-bit LSB-first stream c0 | c1<<6 | c2<<12 | c3<<18, from
 // t = c0 | c1<<8 | c2<<16 | c3<<24 (each code 6 bits): close the byte gaps pairwise.
+// The cvt leaves the top two bits of every code byte zero, so each step is one shift and
+// one bitwise select with complementary masks (a single LOP3): the bits the select takes
+// from the shifted word outside the wanted fields are zero or are dropped by the next step
+// (w bits 14-15 hold c2's low bits; the second select takes w bits 0-11 and 16-27 only).
+template <uint32_t M>
+__device__ __forceinline__ uint32_t sel_bits(uint32_t a, uint32_t b) {   // (a & M) | (b & ~M), one LOP3
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "n"(M));
+  return r;
+}
 __device__ __forceinline__ uint32_t pack6(uint32_t t) {
-  const uint32_t w = (t & 0x003F003Fu) | ((t >> 2) & 0x0FC00FC0u);   // c0|c1<<6 , c2|c3<<6 at bit 16
-  return (w & 0xFFFu) | ((w >> 4) & 0xFFF000u);
+  const uint32_t w = sel_bits<0x003F003Fu>(t, t >> 2);   // c0|c1<<6 , c2|c3<<6 at bit 16
+  return sel_bits<0xFFFu>(w, w >> 4);
 }
 template <> struct Cvt<F_E3M2> {
   static __device__ __forceinline__ uint32_t x4(float a0, float a1, float a2, float a3) {
@@ -163,16 +173,17 @@ __device__ __forceinline__ void encode_store(const ST (&v)[NV], float inv, uint8
       q24[2 * q] = Cvt<FMT>::x4(f[0], f[1], f[2], f[3]);
       q24[2 * q + 1] = Cvt<FMT>::x4(f[4], f[5], f[6], f[7]);
     }
+    // (the 24-bit groups do not overlap: shift-and-add, one IMAD / LEA each)
     if constexpr (NV == 32) {
       uint2* d2 = reinterpret_cast<uint2*>(dst);
-      d2[0] = make_uint2(q24[0] | (q24[1] << 24), (q24[1] >> 8) | (q24[2] << 16));
-      d2[1] = make_uint2((q24[2] >> 16) | (q24[3] << 8), q24[4] | (q24[5] << 24));
-      d2[2] = make_uint2((q24[5] >> 8) | (q24[6] << 16), (q24[6] >> 16) | (q24[7] << 8));
+      d2[0] = make_uint2(q24[1] * 0x1000000u + q24[0], q24[2] * 0x10000u + (q24[1] >> 8));
+      d2[1] = make_uint2(q24[3] * 0x100u + (q24[2] >> 16), q24[5] * 0x1000000u + q24[4]);
+      d2[2] = make_uint2(q24[6] * 0x10000u + (q24[5] >> 8), q24[7] * 0x100u + (q24[6] >> 16));
     } else {  // 12 bytes, 4-byte aligned
       uint32_t* d1 = reinterpret_cast<uint32_t*>(dst);
-      d1[0] = q24[0] | (q24[1] << 24);
-      d1[1] = (q24[1] >> 8) | (q24[2] << 16);
-      d1[2] = (q24[2] >> 16) | (q24[3] << 8);
+      d1[0] = q24[1] * 0x1000000u + q24[0];
+      d1[1] = q24[2] * 0x10000u + (q24[1] >> 8);
+      d1[2] = q24[3] * 0x100u + (q24[2] >> 16);
     }
   } else {  // MXFP8: NV bytes
     uint32_t w[NV / 4];
