@@ -325,14 +325,26 @@ def build_layer(M, K, N, n_sets, device, layer=0, calib_rows=16384, n_shard=None
     return plan, sets
 
 
-def timed_chunks(stream, n_steps, fn, sleep_ms):
+LEAD = int(os.environ.get("BENCH_LEAD", "64"))
+
+
+def timed_chunks(stream, n_steps, fn, sleep_ms, lead=None, mark=None):
     """n_steps calls of fn(i) back to back on `stream`, split into R = min(5, n_steps)
     chunks with one event between chunks, pre-queued behind a device sleep so the
-    events time device execution.  Returns (total ms, [ms per step of each chunk])."""
+    events time device execution.  `lead` untimed calls run between the sleep and the
+    first event: the SM clock drops during the one-thread sleep kernel and needs ~1-2 ms
+    of load to come back, which a short timed region would otherwise absorb.
+    `mark()` (if given) runs between the lead-in and the timed calls.
+    Returns (total ms, [ms per step of each chunk])."""
+    lead = LEAD if lead is None else lead
     R = max(1, min(5, n_steps))
-    bounds = [round(j * n_steps / R) for j in range(R + 1)]
+    bounds = [lead + round(j * n_steps / R) for j in range(R + 1)]
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(R + 1)]
-    torch.cuda._sleep(int(sleep_ms * 1e-3 * 1.9e9))
+    torch.cuda._sleep(int((sleep_ms + 0.3 * lead) * 1e-3 * 1.9e9))
+    for i in range(lead):
+        fn(i)
+    if mark is not None:
+        mark()
     evs[0].record(stream)
     for j in range(R):
         for i in range(bounds[j], bounds[j + 1]):
@@ -349,9 +361,11 @@ def kernel_passes(stream, steps, fn, reps=5):
     out = []
     for _ in range(reps):
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda._sleep(int(min(400.0, 1.0 + 0.2 * steps) * 1e-3 * 1.9e9))
+        torch.cuda._sleep(int(min(400.0, 1.0 + 0.2 * (steps + LEAD)) * 1e-3 * 1.9e9))
+        for i in range(LEAD):   # untimed lead-in launches (clock ramp, see timed_chunks)
+            fn(i)
         k0.record(stream)
-        for i in range(steps):
+        for i in range(LEAD, LEAD + steps):
             fn(i)
         k1.record(stream)
         torch.cuda.synchronize()
@@ -461,12 +475,13 @@ def run_gpu(args, rank, world, local):
         stream.synchronize()
         barrier(world)
         torch.cuda.synchronize()
-        l0 = mm.launch_count()
+        lc = {}
         # K steps back to back (only chunk-boundary events in the stream, so consecutive
         # kernels keep their programmatic-dependent-launch overlap)
-        total_ms, chunk_ms = timed_chunks(stream, args.steps, step, min(400.0, sleep_ms))
+        total_ms, chunk_ms = timed_chunks(stream, args.steps, step, min(400.0, sleep_ms),
+                                          mark=lambda: lc.setdefault("l0", mm.launch_count()))
         barrier(world)
-        launches = mm.launch_count() - l0
+        launches = mm.launch_count() - lc["l0"]
         # per-kernel passes: that kernel's average launch duration over the same rotation
         rq_pass = kernel_passes(stream, args.steps, lambda i: mm.mm_reorder_quantize_act(
             sets[i % n_sets]["x"], plan, out=sets[i % n_sets]["a"], stream=stream))
@@ -667,6 +682,8 @@ def run_gpu(args, rank, world, local):
                    "l2": f"{n_sets} rotating input/weight/output sets, {n_sets * per_set / 1e6:.0f} MB > L2 "
                          f"{l2 / 1e6:.0f} MB (inputs differ from step to step; no L2 flush)",
                    "timing": "CUDA events on the launching stream; steps pre-queued behind a device sleep "
+                             f"and {LEAD} untimed lead-in steps (the SM clock drops during the one-thread sleep "
+                             "kernel and takes ~1-2 ms of load to recover) "
                              "(device time; host enqueue cost is in e2e); value/ms_per_step from the whole region "
                              "(R <= 5 chunks, one event between chunks); per-kernel durations (breakdown, roofline) "
                              "= median of 5 passes of K back-to-back launches of that kernel alone"},
