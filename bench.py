@@ -326,6 +326,7 @@ def build_layer(M, K, N, n_sets, device, layer=0, calib_rows=16384, n_shard=None
 
 
 LEAD = int(os.environ.get("BENCH_LEAD", "64"))
+HOST = {}
 
 
 def timed_chunks(stream, n_steps, fn, sleep_ms, lead=None, mark=None):
@@ -345,11 +346,13 @@ def timed_chunks(stream, n_steps, fn, sleep_ms, lead=None, mark=None):
         fn(i)
     if mark is not None:
         mark()
+    t0 = time.perf_counter()
     evs[0].record(stream)
     for j in range(R):
         for i in range(bounds[j], bounds[j + 1]):
             fn(i)
         evs[j + 1].record(stream)
+    HOST["enqueue_us_per_step"] = (time.perf_counter() - t0) * 1e6 / max(1, n_steps)
     torch.cuda.synchronize()
     per = [evs[j].elapsed_time(evs[j + 1]) / max(1, bounds[j + 1] - bounds[j]) for j in range(R)]
     return evs[0].elapsed_time(evs[R]), per
@@ -482,6 +485,7 @@ def run_gpu(args, rank, world, local):
                                           mark=lambda: lc.setdefault("l0", mm.launch_count()))
         barrier(world)
         launches = mm.launch_count() - lc["l0"]
+        host_us = HOST.get("enqueue_us_per_step")
         # per-kernel passes: that kernel's average launch duration over the same rotation
         rq_pass = kernel_passes(stream, args.steps, lambda i: mm.mm_reorder_quantize_act(
             sets[i % n_sets]["x"], plan, out=sets[i % n_sets]["a"], stream=stream))
@@ -710,6 +714,7 @@ def run_gpu(args, rank, world, local):
                 "pipeline": ("H2D, RQ + GEMM and D2H on three streams over two device slots (copies of "
                              "neighbouring steps overlap compute)" if pipelined else "serial")},
         "gpu_launches": launches,
+        "host_enqueue_us_per_step": host_us,
         "clocks": clocks,
         "cpu_baseline": cpu,
     }
