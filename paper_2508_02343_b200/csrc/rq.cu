@@ -489,38 +489,12 @@ __device__ __forceinline__ void tile_chunks(const RqArgs& a, const ChunkCtx<R>& 
     block_amax<16>(v, am);   // every lane of the warp (full-warp shuffle), before any divergence
     const bool store_sf = live && h == 0;
     if (MM_RQ_EXPERIMENTS && (cx.dbg & 8)) continue;            // experiment: no encode, no stores
-    // One-row tiles: the segment of the chunk's first and last live block are equal
-    // (warp-uniform) except in the chunks that straddle a segment boundary -- uniform
-    // chunks take a path whose segment geometry is compile-time (uniform registers, no
-    // per-lane selects): C4 145.5 -> 142.0 us.  For two-row tiles the extra code and
-    // registers (68 -> 74) cost more than the selects (b8 q/o 38.7 -> 39.3 us): off there.
-    const int bl0 = c * 16, bl1 = min(c * 16 + 15, nbt - 1);
-    const int g0 = bl0 < b1 ? 0 : (bl0 < b2 ? 1 : 2), g1 = bl1 < b1 ? 0 : (bl1 < b2 ? 1 : 2);
-    if (R == 1 && g0 == g1) {
-      if (g0 == 0) encode_uniform<R, 0>(a, v, am, b, h, r0, sf_row, 0, cx.nvalid, live, store_sf, true);
-      else if (g0 == 1) encode_uniform<R, 1>(a, v, am, b, h, r0, sf_row, b1, cx.nvalid, live, store_sf, e3m2);
-      else encode_uniform<R, 2>(a, v, am, b, h, r0, sf_row, b2, cx.nvalid, live, store_sf, e4m3);
-      continue;
-    }
-    const int g = b < b1 ? 0 : (b < b2 ? 1 : 2);
-    const int kb = b - sel3(g, 0, b1, b2);                      // block inside its segment
-    const int hb = sel3(g, 8, 12, 16);                          // code bytes per half block
-    const uint32_t pitch = (uint32_t)sel3(g, (int)a.geom.pitch[0], (int)a.geom.pitch[1], (int)a.geom.pitch[2]);
-    const int kp = sel3(g, a.geom.kp[0], a.geom.kp[1], a.geom.kp[2]);
-    const int off = sel3(g, a.geom.sc_off[0], a.geom.sc_off[1], a.geom.sc_off[2]);
-    uint8_t* const codes = g == 0 ? a.codes[0] : (g == 1 ? a.codes[1] : a.codes[2]);
-    uint8_t* const sf = g == 0 ? a.sf[0] : (g == 1 ? a.sf[1] : a.sf[2]);
-    uint8_t* crow0 = codes + (uint64_t)r0 * pitch + (unsigned)(h * hb) + (unsigned)kb * (2 * hb);
-    uint8_t* sfp = sf + (size_t)((r0 >> 7) * ((unsigned)kp >> 7) + ((unsigned)kb >> 2)) * 512 + sf_row + (kb & 3);
-    if (g == 0) {
-      quantize_rows<R, 0, F_E2M1, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
-    } else if (g == 1) {
-      if (e3m2) quantize_rows<R, 1, F_E3M2, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
-      else quantize_rows<R, 1, F_E2M3, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
-    } else {
-      if (e4m3) quantize_rows<R, 2, F_E4M3, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
-      else quantize_rows<R, 2, F_E5M2, 16>(v, am, off, crow0, pitch, sfp, cx.nvalid, live, store_sf);
-    }
+    // Encode + stores: a per-lane branch on the block's segment (warp-uniform except in the
+    // at most two chunks that straddle a segment boundary); each branch addresses its
+    // segment with compile-time geometry (no per-lane selects of pitch / base / offsets).
+    if (b < b1) encode_uniform<R, 0>(a, v, am, b, h, r0, sf_row, 0, cx.nvalid, live, store_sf, true);
+    else if (b < b2) encode_uniform<R, 1>(a, v, am, b, h, r0, sf_row, b1, cx.nvalid, live, store_sf, e3m2);
+    else encode_uniform<R, 2>(a, v, am, b, h, r0, sf_row, b2, cx.nvalid, live, store_sf, e4m3);
   }
 }
 
