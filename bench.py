@@ -757,7 +757,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gemm-bn", type=int, default=0, help="GEMM tile N override (tuning)")
     ap.add_argument("--gemm-stages", type=int, default=0, help="GEMM pipeline stages override (tuning)")
-    ap.add_argument("--traffic", default="profiles/traffic_r02i.json",
+    ap.add_argument("--traffic", default="profiles/traffic_r02l.json",
                     help="ncu dram bytes per launch (written from an ncu --set full capture)")
     args = ap.parse_args()
     if args.warmup < 3:
