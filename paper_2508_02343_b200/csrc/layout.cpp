@@ -11,8 +11,6 @@
 // transpose's store instructions conflict free (rq.cu) and lets a local search move
 // bank bits 3..4 of every chunk.  Nothing computed changes: only where a value sits in
 // shared memory.  The result is packed one u32 per line: nibble c = position of chunk c.
-// The two-row kernel without the norm also XORs the position with 1 on odd lines (its
-// transpose then needs no per-lane data selects); the bank model below includes that.
 #include <algorithm>
 #include <cstdint>
 #include <vector>
@@ -59,7 +57,7 @@ std::vector<uint32_t> gather_layout(int K, const int n[3], const int32_t* perm) 
       for (int i = 0; i < ns; ++i) dup |= seen[i] == p;
       if (dup) continue;
       seen[ns++] = p;
-      const int bank = (4 * (pos[p >> 2] ^ ((p >> 5) & 1)) + (p & 3)) & 31;   // odd lines: parity flip
+      const int bank = (4 * pos[p >> 2] + (p & 3)) & 31;
       best = std::max(best, ++cnt[bank]);
     }
     return best;
@@ -114,7 +112,7 @@ long long gather_wavefronts(int K, const int n[3], const int32_t* perm, const ui
         if (dup) continue;
         seen[ns++] = p;
         const int ps = layout ? (int)((layout[p >> 5] >> (4 * ((p >> 2) & 7))) & 7) : ((p >> 2) & 7);
-        best = std::max(best, ++cnt[(4 * (ps ^ ((p >> 5) & 1)) + (p & 3)) & 31]);
+        best = std::max(best, ++cnt[(4 * ps + (p & 3)) & 31]);
       }
       tot += best;
     }

@@ -669,11 +669,9 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     // "rotated" slot (q + rot(l)) of its own group (see tile_chunks).
     const uint32_t sz = (uint32_t)sizeof(ST);
     // slot of channel p: the layout moves 4-channel chunks inside each 32-channel line
-    // (LX: odd 32-channel lines flip the chunk parity, see the transpose)
     auto slot = [layout, lay_w](uint32_t p) -> uint32_t {
-      const uint32_t fl = LX ? ((p >> 5) & 1u) : 0u;
-      const uint32_t q = layout ? ((lay_w[p >> 5] >> (4 * ((p >> 2) & 7))) & 7u) : ((p >> 2) & 7u);
-      return (p & ~31u) | ((q ^ fl) << 2) | (p & 3u);
+      if (!layout) return p;
+      return (p & ~31u) | (((lay_w[p >> 5] >> (4 * ((p >> 2) & 7))) & 7u) << 2) | (p & 3u);
     };
     if (layout && !LX)   // one word per 32-channel line of every box; lines past K keep the natural order
       for (int t = ct; t < 8 * nbox; t += cn) lay_s[t] = t < K / 32 ? __ldg(layout + t) : 0x76543210u;
@@ -712,25 +710,23 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     }
   }
   if constexpr (LX) {
-    // Transpose store offsets: for lane l of box b, the byte offsets inside the box of its
-    // even and its odd 16-byte chunk (low / high half).  Lane l owns chunks 2 (l & 3) and
-    // 2 (l & 3) + 1 of 32-channel line l / 4; their positions come from the plan's
-    // parity-preserving gather layout (natural order without one and past K), XOR 1 on odd
-    // lines: each store instruction (all lanes' even chunks, then all odd ones) then fills
-    // 8 bank groups per 8 lanes (even lines at even positions, odd lines at odd ones)
-    // without any per-lane data select, and the row reads are whole 16-byte vectors.
+    // Transpose store offsets: for lane l of box b, the byte offsets inside the box of its two
+    // 16-byte chunks, the one stored first in the low half.  Lane l owns chunks 2 (l & 3) and
+    // 2 (l & 3) + 1 of 32-channel line l / 4; lanes 4..7 of every 8 store their odd chunk
+    // first (8 bank groups per store instruction); the chunk positions come from the plan's
+    // parity-preserving gather layout (natural order without one and past K).
     const int ct = threadIdx.x - 32, cn = groups * group_warps * 32;
     for (int t = ct; t < 32 * nbox; t += cn) {
       const int l = t & 31, li = 8 * (t >> 5) + (l >> 2);
-      const uint32_t qe = 2u * (uint32_t)(l & 3), fl = (uint32_t)li & 1u;
-      uint32_t pe = qe, po = qe + 1u;
+      const uint32_t qf = 2u * (uint32_t)(l & 3) + (uint32_t)((l >> 2) & 1);
+      uint32_t pf = qf, ps = qf ^ 1u;
       if (layout && li < K / 32) {
         const uint32_t lw = lay_w[li];
-        pe = (lw >> (4 * qe)) & 7u;
-        po = (lw >> (4 * (qe + 1u))) & 7u;
+        pf = (lw >> (4 * qf)) & 7u;
+        ps = (lw >> (4 * (qf ^ 1u))) & 7u;
       }
       const uint32_t base = (uint32_t)(l >> 2) * 128u;
-      lay_s[t] = (base + 16u * (pe ^ fl)) | ((base + 16u * (po ^ fl)) << 16);
+      lay_s[t] = (base + 16u * pf) | ((base + 16u * ps) << 16);
     }
   }
   if (tab || LX) {
@@ -765,24 +761,30 @@ rq_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ RqDev
     double nhi[4] = {0, 0, 0, 0}, nlo[4] = {0, 0, 0, 0};
     if constexpr (R > 1) {
       if constexpr (LX) {
-        // Lane l owns channels 8 l .. 8 l + 7 of each box: one 16-byte read per row, the two
-        // transposed 16-byte chunks stored at the offsets lay_s holds for (box, lane).
-        // Shared addresses are 32-bit with a warp-uniform box base.
-        const uint32_t rl = (uint32_t)lane * 16u;
+        // Lane l owns channels 8 l .. 8 l + 7 of each box; it reads its row words as two
+        // 8-byte halves in store order (no register selects) and stores the two transposed
+        // 16-byte chunks at the offsets lay_s holds for (box, lane).  Shared addresses are
+        // 32-bit with a warp-uniform box base.
+        const uint32_t f8 = 8u * (uint32_t)((lane >> 2) & 1);
+        const uint32_t rf = (uint32_t)lane * 16u + f8, rs = (uint32_t)lane * 16u + (f8 ^ 8u);
         const uint32_t st_b = __reduce_max_sync(0xffffffffu, ptx::smem_u32(st));
         const uint32_t lx = ptx::smem_u32(lay_s) + 4u * (uint32_t)lane;
         for (int b = gw; b < nbox && !(dbg & 2); b += group_warps) {
           const uint32_t box = st_b + (uint32_t)b * 1024u;
-          const uint4 x0 = lds_u4(box + rl), x1 = lds_u4(box + rl + 512u);
+          uint2 a0, a1, b0, b1;
+          asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(a0.x), "=r"(a0.y) : "r"(box + rf));
+          asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+512];" : "=r"(a1.x), "=r"(a1.y) : "r"(box + rf));
+          asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(b0.x), "=r"(b0.y) : "r"(box + rs));
+          asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+512];" : "=r"(b1.x), "=r"(b1.y) : "r"(box + rs));
           uint32_t w;
           asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w) : "r"(lx + (uint32_t)b * 128u));
           __syncwarp();
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + (w & 0xFFFFu)),
-                       "r"(__byte_perm(x0.x, x1.x, 0x5410)), "r"(__byte_perm(x0.x, x1.x, 0x7632)),
-                       "r"(__byte_perm(x0.y, x1.y, 0x5410)), "r"(__byte_perm(x0.y, x1.y, 0x7632)) : "memory");
+                       "r"(__byte_perm(a0.x, a1.x, 0x5410)), "r"(__byte_perm(a0.x, a1.x, 0x7632)),
+                       "r"(__byte_perm(a0.y, a1.y, 0x5410)), "r"(__byte_perm(a0.y, a1.y, 0x7632)) : "memory");
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + (w >> 16)),
-                       "r"(__byte_perm(x0.z, x1.z, 0x5410)), "r"(__byte_perm(x0.z, x1.z, 0x7632)),
-                       "r"(__byte_perm(x0.w, x1.w, 0x5410)), "r"(__byte_perm(x0.w, x1.w, 0x7632)) : "memory");
+                       "r"(__byte_perm(b0.x, b1.x, 0x5410)), "r"(__byte_perm(b0.x, b1.x, 0x7632)),
+                       "r"(__byte_perm(b0.y, b1.y, 0x5410)), "r"(__byte_perm(b0.y, b1.y, 0x7632)) : "memory");
         }
       } else
       for (int b = gw; b < nbox && !(dbg & 2); b += group_warps) {
